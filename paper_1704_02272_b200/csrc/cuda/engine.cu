@@ -1,0 +1,611 @@
+// engine.cu -- host runtime of the GPU match engine: device images of tries,
+// pooled per-call workspaces (stream, buffers, tile status), the streaming
+// H2D -> kernel -> D2H pipeline behind hepfac_scan, run_throughput and the
+// device-resident benchmark session.  No CPU fallback: without a usable
+// sm_100a device every entry point fails with HEPFAC_ERR_INTERNAL.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../host/image.hpp"
+#include "engine.hpp"
+#include "scan_kernel.cuh"
+
+namespace hfb {
+
+// ---------------------------------------------------------------------------
+// errors
+
+namespace {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what)
+{
+    const hepfac_status_t s = e == cudaErrorMemoryAllocation ? HEPFAC_ERR_NOMEM : HEPFAC_ERR_INTERNAL;
+    fail(s, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x)                                      \
+    do {                                           \
+        cudaError_t e_ = (x);                      \
+        if (e_ != cudaSuccess) cuda_fail(e_, #x);  \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d)
+    {
+        cudaGetDevice(&prev);
+        if (prev != d) CK(cudaSetDevice(d));
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int pick_device()
+{
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        fail(HEPFAC_ERR_INTERNAL,
+             "no CUDA device available: the B200 build of hepfac matches on the GPU only "
+             "(no CPU fallback)");
+    }
+    int d = 0;
+    if (const char* s = std::getenv("HEPFAC_DEVICE")) d = std::atoi(s);
+    else cudaGetDevice(&d);
+    if (d < 0 || d >= n) invalid("HEPFAC_DEVICE out of range");
+    return d;
+}
+
+template <typename T>
+T* dev_alloc(size_t count)
+{
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+} // namespace
+
+int device_count()
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------------------
+// MatchList
+
+MatchList::~MatchList() { std::free(data); }
+
+void MatchList::allocate(size_t n)
+{
+    std::free(data);
+    data = nullptr;
+    size = n;
+    if (n == 0) return;
+    data = static_cast<hepfac_match_t*>(std::malloc(n * sizeof(hepfac_match_t)));
+    if (!data) throw std::bad_alloc();
+}
+
+// ---------------------------------------------------------------------------
+// Device image of a trie
+
+using KernelFn = void (*)(gpu::ScanArgs);
+
+struct DeviceTrie {
+    int device = 0;
+    std::vector<void*> allocs;
+    TrieView view{};
+    bool grouped = false, identity = false;
+    int kw = 0;
+    KernelFn kernel = nullptr;
+    size_t smem = 0;
+    int blocks_per_sm = 1, sm_count = 1;
+    uint32_t min_emit = UINT32_MAX, node_count = 0, groups = 0;
+    uint64_t reach = 0, filter_paths = 0, device_bytes = 0, private_terminals = 0, keyed_terminals = 0;
+
+    template <typename T>
+    const T* upload(const std::vector<T>& v)
+    {
+        T* d = dev_alloc<T>(v.size());
+        allocs.push_back(d);
+        if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        return d;
+    }
+
+    ~DeviceTrie()
+    {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+KernelFn select_kernel(bool grouped, bool identity, int kw)
+{
+    using namespace gpu;
+    // identity byte maps only exist at sigma = 256, i.e. the grouped layout
+    static const KernelFn table[2][2][3] = {
+        {{pfac_scan_kernel<false, false, 0>, pfac_scan_kernel<false, false, 1>, pfac_scan_kernel<false, false, 2>},
+         {pfac_scan_kernel<false, false, 0>, pfac_scan_kernel<false, false, 1>, pfac_scan_kernel<false, false, 2>}},
+        {{pfac_scan_kernel<true, false, 0>, pfac_scan_kernel<true, false, 1>, pfac_scan_kernel<true, false, 2>},
+         {pfac_scan_kernel<true, true, 0>, pfac_scan_kernel<true, true, 1>, pfac_scan_kernel<true, true, 2>}}};
+    return table[grouped][identity && grouped][kw];
+}
+
+std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
+{
+    DeviceGuard g(device);
+    const GpuImage im = build_gpu_image(t, image_options_from_env());
+    auto d = std::make_shared<DeviceTrie>();
+    d->device = device;
+    d->grouped = im.groups != 0;
+    d->identity = im.identity && d->grouped;
+    d->kw = im.filter_bits == 0 ? 0 : (im.filter_k <= 4 ? 1 : 2);
+    d->min_emit = im.min_emit;
+    d->reach = im.reach;
+    d->node_count = im.node_count;
+    d->groups = im.groups;
+    d->filter_paths = im.filter_paths;
+    d->device_bytes = im.device_bytes();
+    d->private_terminals = im.private_terminals;
+    d->keyed_terminals = im.keyed_terminals;
+
+    TrieView& v = d->view;
+    v.nodes = d->upload(im.nodes);
+    v.term_id = d->upload(im.term_id);
+    v.bucket_of = d->upload(im.bucket_of);
+    v.groups = im.groups;
+    v.depth_limit = im.depth_limit;
+    v.symtab = d->upload(std::vector<uint16_t>(im.symtab.begin(), im.symtab.end()));
+    v.pat_bytes = d->upload(im.pat_bytes);
+    v.pat_off = d->upload(im.pat_off);
+    v.pat_len = d->upload(im.pat_len);
+    v.ht_key = d->upload(im.ht_key);
+    v.ht_id = d->upload(im.ht_id);
+    v.ht_mask = im.ht_mask;
+    v.hmul = im.hmul;
+    v.bk_start = d->upload(im.bk_start);
+    v.bk_ids = d->upload(im.bk_ids);
+    v.filter = d->upload(im.filter);
+    v.filter_words = d->kw ? uint32_t(im.filter.size()) : 0u;
+    v.filter_bits = im.filter_bits;
+    v.filter_k = im.filter_k;
+    v.min_emit = im.min_emit;
+
+    d->kernel = select_kernel(d->grouped, d->identity, d->kw);
+    d->smem = size_t(v.filter_words) * 4 + (d->identity ? 0 : 512) + gpu::kSmemText;
+    CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
+    d->blocks_per_sm = std::max(1, d->blocks_per_sm);
+    CK(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device));
+    return d;
+}
+
+} // namespace
+
+Trie::~Trie() = default;
+
+std::shared_ptr<DeviceTrie> Trie::device_image(int device) const
+{
+    std::lock_guard<std::mutex> lk(dev_mu_);
+    if (dev_.size() <= size_t(device)) dev_.resize(size_t(device) + 1);
+    if (!dev_[device]) dev_[device] = make_device_trie(*this, device);
+    return dev_[device];
+}
+
+// ---------------------------------------------------------------------------
+// Workspaces: one stream + buffers per concurrent call, pooled per device.
+
+namespace {
+
+struct Workspace {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {};
+    uint8_t* d_text = nullptr;
+    size_t text_cap = 0;
+    hepfac_match_t* d_out = nullptr;
+    uint64_t out_cap = 0;
+    unsigned long long* d_status = nullptr;
+    uint64_t status_cap = 0;
+    unsigned long long* d_small = nullptr; // [0] tile counter, [1] total, [2] error word
+    unsigned long long* h_small = nullptr; // pinned mirror of [1], [2]
+    unsigned long long ctr_base = 0;
+    uint32_t epoch = 0;
+    uint4* d_flush = nullptr;
+    size_t flush_n16 = 0;
+
+    explicit Workspace(int dev) : device(dev)
+    {
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        d_small = dev_alloc<unsigned long long>(4);
+        CK(cudaMemset(d_small, 0, 4 * sizeof(unsigned long long)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_small), 4 * sizeof(unsigned long long), cudaHostAllocDefault));
+    }
+    ~Workspace()
+    {
+        cudaSetDevice(device);
+        cudaStreamSynchronize(stream);
+        cudaFree(d_text);
+        cudaFree(d_out);
+        cudaFree(d_status);
+        cudaFree(d_small);
+        cudaFree(d_flush);
+        cudaFreeHost(h_small);
+        for (auto& e : ev) cudaEventDestroy(e);
+        cudaStreamDestroy(stream);
+    }
+
+    void ensure_text(size_t bytes)
+    {
+        const size_t need = ((bytes + 15) & ~size_t(15)) + 16;
+        if (need <= text_cap) return;
+        cudaFree(d_text);
+        d_text = nullptr;
+        text_cap = 0;
+        d_text = dev_alloc<uint8_t>(need);
+        text_cap = need;
+    }
+    void ensure_out(uint64_t n)
+    {
+        if (n <= out_cap) return;
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(d_out);
+        d_out = nullptr;
+        out_cap = 0;
+        d_out = dev_alloc<hepfac_match_t>(size_t(n));
+        out_cap = n;
+    }
+    void ensure_status(uint64_t tiles)
+    {
+        if (tiles <= status_cap) return;
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(d_status);
+        d_status = nullptr;
+        status_cap = 0;
+        d_status = dev_alloc<unsigned long long>(size_t(tiles));
+        CK(cudaMemset(d_status, 0, size_t(tiles) * sizeof(unsigned long long)));
+        status_cap = tiles;
+        epoch = 0;
+    }
+};
+
+std::mutex g_pool_mu;
+std::vector<std::vector<std::unique_ptr<Workspace>>> g_pool;
+
+struct WorkspaceLease {
+    std::unique_ptr<Workspace> ws;
+    explicit WorkspaceLease(int dev)
+    {
+        {
+            std::lock_guard<std::mutex> lk(g_pool_mu);
+            if (g_pool.size() <= size_t(dev)) g_pool.resize(size_t(dev) + 1);
+            if (!g_pool[dev].empty()) {
+                ws = std::move(g_pool[dev].back());
+                g_pool[dev].pop_back();
+            }
+        }
+        if (!ws) ws = std::make_unique<Workspace>(dev);
+    }
+    ~WorkspaceLease()
+    {
+        if (!ws) return;
+        if (cudaStreamSynchronize(ws->stream) != cudaSuccess) {
+            cudaGetLastError();
+            return; // poisoned: drop it
+        }
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_pool[ws->device].push_back(std::move(ws));
+    }
+    Workspace* operator->() { return ws.get(); }
+    Workspace& operator*() { return *ws; }
+};
+
+thread_local ScanStats t_stats;
+
+// Enqueue one kernel launch over device-resident text.  The tile counter is
+// never reset: each launch consumes exactly n_tiles + grid increments.
+uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text, uint64_t n_own,
+                      uint64_t n_avail, uint64_t g0, hepfac_match_t* d_out, uint64_t cap)
+{
+    const uint64_t n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
+    if (n_tiles == 0) {
+        CK(cudaMemsetAsync(ws.d_small + 1, 0, sizeof(unsigned long long), ws.stream));
+        return 0;
+    }
+    ws.ensure_status(n_tiles);
+    if (++ws.epoch == 0x10000u) {
+        CK(cudaMemsetAsync(ws.d_status, 0, size_t(ws.status_cap) * sizeof(unsigned long long), ws.stream));
+        ws.epoch = 1;
+    }
+    const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(dt.sm_count) * dt.blocks_per_sm);
+    gpu::ScanArgs a{};
+    a.trie = dt.view;
+    a.text = d_text;
+    a.n_own = n_own;
+    a.n_avail = n_avail;
+    a.g0 = g0;
+    a.out = d_out;
+    a.out_cap = cap;
+    a.status = ws.d_status;
+    a.tile_ctr = ws.d_small;
+    a.tile_base = ws.ctr_base;
+    a.n_tiles = n_tiles;
+    a.epoch_bits = (unsigned long long)ws.epoch << 48;
+    a.total = ws.d_small + 1;
+    a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
+    dt.kernel<<<unsigned(grid), gpu::kThreads, dt.smem, ws.stream>>>(a);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        // the counter state is unknown after a failed launch: reset it
+        cudaMemset(ws.d_small, 0, sizeof(unsigned long long));
+        ws.ctr_base = 0;
+        cuda_fail(e, "pfac_scan_kernel launch");
+    }
+    ws.ctr_base += n_tiles + grid;
+    return 1;
+}
+
+void fetch_small(Workspace& ws)
+{
+    CK(cudaMemcpyAsync(ws.h_small, ws.d_small + 1, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    if (ws.h_small[1] & 1u)
+        fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
+}
+
+uint64_t initial_capacity(uint64_t bytes) { return std::max<uint64_t>(1u << 16, bytes / 64); }
+
+double elapsed_ms(cudaEvent_t a, cudaEvent_t b)
+{
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return double(ms);
+}
+
+// Copies `text` in, scans, copies the sorted list out.  The whole text goes to
+// the device in one piece (HBM holds 180 GB); the H2D copy, kernel and D2H
+// run back to back on one stream.
+std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,
+                                         uint64_t g0)
+{
+    auto out = std::make_unique<MatchList>();
+    ScanStats st;
+    st.bytes = owned;
+    if (owned == 0) {
+        t_stats = st;
+        return out;
+    }
+    const int dev = pick_device();
+    st.device = dev;
+    DeviceGuard g(dev);
+    auto dt = t.device_image(dev);
+    if (dt->min_emit == UINT32_MAX || avail < dt->min_emit) {
+        t_stats = st;
+        return out;
+    }
+    WorkspaceLease ws(dev);
+    ws->ensure_text(avail);
+    ws->ensure_out(std::max(ws->out_cap, initial_capacity(owned)));
+    CK(cudaMemsetAsync(ws->d_small + 2, 0, sizeof(unsigned long long), ws->stream));
+    CK(cudaEventRecord(ws->ev[0], ws->stream));
+    CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
+    CK(cudaEventRecord(ws->ev[1], ws->stream));
+    st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0, ws->d_out, ws->out_cap);
+    CK(cudaEventRecord(ws->ev[2], ws->stream));
+    fetch_small(*ws);
+    uint64_t total = ws->h_small[0];
+    if (total > ws->out_cap) { // overflow: re-run with the exact size
+        ws->ensure_out(total);
+        CK(cudaEventRecord(ws->ev[1], ws->stream));
+        st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0, ws->d_out, ws->out_cap);
+        CK(cudaEventRecord(ws->ev[2], ws->stream));
+        fetch_small(*ws);
+        total = ws->h_small[0];
+        st.relaunches = 1;
+    }
+    out->allocate(size_t(total));
+    if (total)
+        CK(cudaMemcpyAsync(out->data, ws->d_out, size_t(total) * sizeof(hepfac_match_t), cudaMemcpyDeviceToHost,
+                           ws->stream));
+    CK(cudaEventRecord(ws->ev[3], ws->stream));
+    CK(cudaStreamSynchronize(ws->stream));
+    st.h2d_ms = elapsed_ms(ws->ev[0], ws->ev[1]);
+    st.kernel_ms = elapsed_ms(ws->ev[1], ws->ev[2]);
+    st.d2h_ms = elapsed_ms(ws->ev[2], ws->ev[3]);
+    st.total_ms = elapsed_ms(ws->ev[0], ws->ev[3]);
+    st.matches = total;
+    st.chunks = 1;
+    t_stats = st;
+    return out;
+}
+
+} // namespace
+
+const ScanStats& last_scan_stats() { return t_stats; }
+
+std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t bytes)
+{
+    return scan_resident(t, text, bytes, bytes, 0);
+}
+
+std::unique_ptr<MatchList> gpu_scan_shard(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,
+                                          uint64_t g0)
+{
+    if (owned > avail) invalid("shard owns more starts than it has bytes");
+    return scan_resident(t, text, avail, owned, g0);
+}
+
+uint64_t gpu_halo(const Trie& t)
+{
+    const int dev = pick_device();
+    auto dt = t.device_image(dev);
+    return dt->reach == UINT64_MAX ? UINT64_MAX : (dt->reach ? dt->reach - 1 : 0);
+}
+
+LayoutInfo layout_info(const Trie& t)
+{
+    const int dev = pick_device();
+    auto d = t.device_image(dev);
+    LayoutInfo li{};
+    li.node_count = d->node_count;
+    li.groups = d->groups;
+    li.record_bytes = d->groups ? 16 * d->groups : 8;
+    li.filter_k = d->view.filter_k;
+    li.filter_bits = d->view.filter_bits;
+    li.min_emit = d->min_emit;
+    li.smem_bytes = uint32_t(d->smem);
+    li.blocks_per_sm = uint32_t(d->blocks_per_sm);
+    li.sm_count = uint32_t(d->sm_count);
+    li.identity = d->identity;
+    li.filter_paths = d->filter_paths;
+    li.reach = d->reach;
+    li.device_bytes = d->device_bytes;
+    li.private_terminals = d->private_terminals;
+    li.keyed_terminals = d->keyed_terminals;
+    return li;
+}
+
+// ---------------------------------------------------------------------------
+// run_throughput (reference bench.cpp:52-78)
+
+Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes, uint32_t runs)
+{
+    if (runs < 1) invalid("runs must be >= 1");
+    if (bytes == 0) invalid("empty corpus");
+    Throughput r;
+    const int dev = pick_device();
+    DeviceGuard g(dev);
+    auto dt = t.device_image(dev);
+    WorkspaceLease ws(dev);
+    ws->ensure_text(bytes);
+    CK(cudaMemcpy(ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
+    if (dt->min_emit == UINT32_MAX || bytes < dt->min_emit) return r;
+    ws->ensure_out(std::max(ws->out_cap, initial_capacity(bytes)));
+    CK(cudaMemsetAsync(ws->d_small + 2, 0, sizeof(unsigned long long), ws->stream));
+    enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0, ws->d_out, ws->out_cap); // warm-up, untimed
+    fetch_small(*ws);
+    ws->ensure_out(ws->h_small[0]);
+    std::vector<hepfac_match_t> host;
+    double sum_scan = 0, sum_merge = 0;
+    for (uint32_t i = 0; i < runs; ++i) {
+        CK(cudaEventRecord(ws->ev[0], ws->stream));
+        enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0, ws->d_out, ws->out_cap);
+        CK(cudaEventRecord(ws->ev[1], ws->stream));
+        fetch_small(*ws);
+        r.matches = ws->h_small[0];
+        host.resize(size_t(r.matches));
+        CK(cudaEventRecord(ws->ev[2], ws->stream));
+        if (r.matches)
+            CK(cudaMemcpyAsync(host.data(), ws->d_out, size_t(r.matches) * sizeof(hepfac_match_t),
+                               cudaMemcpyDeviceToHost, ws->stream));
+        CK(cudaEventRecord(ws->ev[3], ws->stream));
+        CK(cudaStreamSynchronize(ws->stream));
+        sum_scan += elapsed_ms(ws->ev[0], ws->ev[1]) / 1e3;
+        sum_merge += elapsed_ms(ws->ev[2], ws->ev[3]) / 1e3;
+    }
+    r.seconds = sum_scan / runs;
+    r.merge_seconds = sum_merge / runs;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident benchmark session
+
+struct Session {
+    std::shared_ptr<DeviceTrie> dt;
+    std::unique_ptr<Workspace> ws;
+    uint64_t bytes = 0, matches = 0;
+    std::vector<cudaEvent_t> evs;
+    ~Session()
+    {
+        if (!ws) return;
+        cudaSetDevice(ws->device);
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+};
+
+Session* session_create(const Trie& t, const uint8_t* text, uint64_t bytes)
+{
+    if (bytes == 0) invalid("empty corpus");
+    const int dev = pick_device();
+    DeviceGuard g(dev);
+    auto s = std::make_unique<Session>();
+    s->dt = t.device_image(dev);
+    s->ws = std::make_unique<Workspace>(dev);
+    s->bytes = bytes;
+    s->ws->ensure_text(bytes);
+    CK(cudaMemcpy(s->ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
+    s->ws->ensure_out(initial_capacity(bytes));
+    return s.release();
+}
+
+void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
+{
+    Workspace& ws = *s->ws;
+    DeviceGuard g(ws.device);
+    const DeviceTrie& dt = *s->dt;
+    const bool can_match = dt.min_emit != UINT32_MAX && s->bytes >= dt.min_emit;
+    if (flush_l2 && !ws.d_flush) {
+        int l2 = 0;
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ws.device));
+        ws.flush_n16 = size_t(l2) * 2 / 16;
+        ws.d_flush = dev_alloc<uint4>(ws.flush_n16);
+    }
+    while (s->evs.size() < 2 * size_t(iterations)) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        s->evs.push_back(e);
+    }
+    CK(cudaMemsetAsync(ws.d_small + 2, 0, sizeof(unsigned long long), ws.stream));
+    for (uint32_t i = 0; i < iterations; ++i) {
+        if (flush_l2)
+            gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
+        CK(cudaEventRecord(s->evs[2 * i], ws.stream));
+        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->bytes, s->bytes, 0, ws.d_out, ws.out_cap);
+        CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
+    }
+    fetch_small(ws);
+    s->matches = can_match ? ws.h_small[0] : 0;
+    for (uint32_t i = 0; i < iterations; ++i)
+        if (ms_each) ms_each[i] = elapsed_ms(s->evs[2 * i], s->evs[2 * i + 1]);
+    if (s->matches > ws.out_cap) ws.ensure_out(s->matches); // next run stores everything
+}
+
+uint64_t session_matches(Session* s) { return s->matches; }
+
+std::unique_ptr<MatchList> session_fetch(Session* s)
+{
+    Workspace& ws = *s->ws;
+    DeviceGuard g(ws.device);
+    if (s->matches > ws.out_cap) fail(HEPFAC_ERR_STATE, "session results overflowed: run again before fetching");
+    auto out = std::make_unique<MatchList>();
+    out->allocate(size_t(s->matches));
+    if (s->matches)
+        CK(cudaMemcpy(out->data, ws.d_out, size_t(s->matches) * sizeof(hepfac_match_t), cudaMemcpyDeviceToHost));
+    return out;
+}
+
+void session_destroy(Session* s) { delete s; }
+
+} // namespace hfb

@@ -1,0 +1,80 @@
+// layout.hpp -- the GPU image of a trie, shared by the host builder (g++)
+// and the sm_100a kernels (nvcc).
+//
+// Node records (node indices are the canonical ones, so a GPU node id is the
+// same number hepfac_trie_transition returns):
+//   narrow  (sigma <= 32) : uint2 {bitmap, base|flags}                 8 B/node
+//   grouped (sigma >  32) : per 64-symbol group g a uint4
+//                           {bitmap[2g], bitmap[2g+1], base_g|flags, term_id}
+//                           16 B per group: 16/32/64 B for sigma 64/128/256
+// base_g = first-child index + popcount of all bitmap words before group g,
+// so ONE 16-byte load per text byte resolves a transition (reference Eq. 1,
+// trie.hpp:68-79, needs up to 8 dependent word reads at sigma = 256).
+// flags: bit 31 terminal, bit 30 carries a verification bucket.
+#pragma once
+
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define HFB_HD __host__ __device__ __forceinline__
+#else
+#define HFB_HD inline
+#endif
+
+namespace hfb {
+
+constexpr uint32_t kFlagTerminal = 0x80000000u;
+constexpr uint32_t kFlagBucket = 0x40000000u;
+constexpr uint32_t kBaseMask = 0x3FFFFFFFu;
+constexpr uint32_t kMaxGpuNodes = 0x40000000u;
+constexpr uint32_t kNoId = 0xFFFFFFFFu;
+constexpr uint16_t kNoSym = 0xFFFFu;
+constexpr uint32_t kMaxFilterKey = 8; // bytes hashed by the start filter
+
+// Rolling hash of a byte string (1-based bytes so 0x00 counts), mixed with
+// the length: the dictionary key of a matched slice.
+HFB_HD uint64_t slice_step(uint64_t h, uint64_t mul, uint32_t byte) { return h * mul + byte + 1; }
+HFB_HD uint64_t slice_key(uint64_t h, uint32_t len) { return h ^ (uint64_t(len) * 0x9E3779B97F4A7C15ull); }
+HFB_HD uint64_t mix64(uint64_t k)
+{
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+// Start filter: the first k text bytes (little-endian packed) hashed to a
+// 2^bits bitmap.  k <= 4 uses a 32-bit multiply, k <= 8 a 64-bit one.
+HFB_HD uint32_t filter_slot32(uint32_t key, uint32_t bits) { return (key * 0x9E3779B1u) >> (32 - bits); }
+HFB_HD uint32_t filter_slot64(uint64_t key, uint32_t bits)
+{
+    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+}
+
+// Device view of an uploaded image (plain pointers, passed by value).
+struct TrieView {
+    const uint32_t* nodes;
+    const uint32_t* term_id;   // per node: private pattern id, or kNoId = resolve by key
+    const uint32_t* bucket_of; // per node: bucket index or kNoId
+    uint32_t groups;           // grouped format: uint4 records per node
+    uint32_t depth_limit;      // 0 = untruncated
+    const uint16_t* symtab;    // [256], kNoSym = byte outside the alphabet
+    const uint8_t* pat_bytes;
+    const uint64_t* pat_off;
+    const uint32_t* pat_len;
+    const uint64_t* ht_key;
+    const uint32_t* ht_id;
+    uint64_t ht_mask;
+    uint64_t hmul;
+    const uint32_t* bk_start;
+    const uint32_t* bk_ids;
+    const uint32_t* filter;
+    uint32_t filter_words;
+    uint32_t filter_bits; // 0 = filter disabled (every start walks)
+    uint32_t filter_k;
+    uint32_t min_emit;
+};
+
+} // namespace hfb

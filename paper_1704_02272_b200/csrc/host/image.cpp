@@ -1,0 +1,294 @@
+// image.cpp -- canonical trie -> GPU image.
+//
+// What the kernel needs that the canonical cells do not give directly:
+//   * one-load transitions (grouped records with per-group rank bases);
+//   * pattern ids at terminals.  The reference hashes the matched slice into
+//     its dictionary (trie.hpp:103-107) because stage-1/2 terminals are shared
+//     (SPEC.md:368).  Here every terminal reached by exactly one root path gets
+//     its id baked in; shared terminals resolve by a 64-bit slice key into an
+//     open-addressing table, followed by a byte compare;
+//   * verification buckets as a CSR sorted by (length, id), so a start's
+//     matches come out already in (length, id) order (scan.hpp:17-23);
+//   * the start filter: every start that can report passes through a node at
+//     depth k = min(8, shortest report depth), so the set of depth-k path
+//     strings, hashed into a bitmap, rejects most starts with one shared-memory
+//     probe;
+//   * reach, the longest byte span one start can read (the halo of a shard).
+#include "image.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <unordered_set>
+
+namespace hfb {
+
+size_t GpuImage::device_bytes() const
+{
+    return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
+           pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
+           bk_start.size() * 4 + bk_ids.size() * 4 + filter.size() * 4 + 512;
+}
+
+ImageOptions image_options_from_env()
+{
+    ImageOptions o;
+    if (const char* s = std::getenv("HEPFAC_FILTER_BITS_MAX")) {
+        long v = std::strtol(s, nullptr, 10);
+        if (v >= 10 && v <= 20) o.max_filter_bits = uint32_t(v);
+    }
+    if (const char* s = std::getenv("HEPFAC_FILTER_SLACK")) {
+        long v = std::strtol(s, nullptr, 10);
+        if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
+    }
+    return o;
+}
+
+namespace {
+
+uint32_t ceil_log2(uint64_t x)
+{
+    uint32_t b = 0;
+    while ((uint64_t(1) << b) < x) ++b;
+    return b;
+}
+
+} // namespace
+
+GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
+{
+    GpuImage im;
+    const uint32_t n = t.node_count;
+    if (n >= kMaxGpuNodes) fail(HEPFAC_ERR_NOMEM, "trie too large for the GPU image (>= 2^30 nodes)");
+    im.node_count = n;
+
+    // Structural validation: a loaded .htri is only checked for offset < n by
+    // the format (reference trie_io.cpp:155-159); child runs must fit too.
+    std::vector<uint32_t> kids(n);
+    for (uint32_t u = 0; u < n; ++u) {
+        kids[u] = t.child_count(u);
+        if (kids[u] && uint64_t(t.offset(u)) + kids[u] > n)
+            fail(HEPFAC_ERR_FORMAT, "trie file offset out of range (child run past the node array)");
+    }
+
+    // ---- alphabet --------------------------------------------------------
+    im.identity = t.alphabet.is_identity();
+    for (unsigned b = 0; b < 256; ++b) {
+        int s = t.alphabet.symbol_of(uint8_t(b));
+        im.symtab[b] = s < 0 ? kNoSym : uint16_t(s);
+    }
+    im.depth_limit = t.depth_limit.value_or(0);
+
+    // ---- dictionary + slice-key table -------------------------------------
+    const size_t P = t.patterns.size();
+    im.pat_off.resize(P);
+    im.pat_len.resize(P);
+    for (size_t i = 0; i < P; ++i) {
+        im.pat_off[i] = im.pat_bytes.size();
+        im.pat_len[i] = uint32_t(t.patterns[i].size());
+        im.pat_bytes.insert(im.pat_bytes.end(), t.patterns[i].begin(), t.patterns[i].end());
+    }
+    if (im.pat_bytes.empty()) im.pat_bytes.push_back(0);
+    std::vector<uint64_t> keys(P);
+    for (uint64_t attempt = 0;; ++attempt) {
+        im.hmul = 0x100000001B3ull + 2 * attempt * 0x9E3779B97F4A7C15ull; // odd multipliers
+        std::unordered_set<uint64_t> seen;
+        seen.reserve(P * 2);
+        bool unique = true;
+        for (size_t i = 0; i < P && unique; ++i) {
+            uint64_t h = 0;
+            for (unsigned char c : t.patterns[i]) h = slice_step(h, im.hmul, c);
+            keys[i] = slice_key(h, uint32_t(t.patterns[i].size()));
+            unique = seen.insert(keys[i]).second;
+        }
+        if (unique) break;
+        if (attempt > 64) fail(HEPFAC_ERR_INTERNAL, "cannot find collision-free slice keys");
+    }
+    const uint64_t slots = uint64_t(1) << std::max<uint32_t>(4, ceil_log2(2 * P + 1));
+    im.ht_mask = slots - 1;
+    im.ht_key.assign(slots, 0);
+    im.ht_id.assign(slots, kNoId);
+    for (size_t i = 0; i < P; ++i) {
+        uint64_t s = mix64(keys[i]) & im.ht_mask;
+        while (im.ht_id[s] != kNoId) s = (s + 1) & im.ht_mask;
+        im.ht_key[s] = keys[i];
+        im.ht_id[s] = uint32_t(i);
+    }
+
+    // ---- terminal ids: baked in where the node spells exactly one string ----
+    std::vector<uint32_t> indeg(n, 0);
+    for (uint32_t u = 0; u < n; ++u)
+        for (uint32_t i = 0; i < kids[u]; ++i) indeg[t.offset(u) + i]++;
+    std::vector<uint8_t> unique_path(n, 0);
+    {
+        std::vector<uint32_t> q{0};
+        unique_path[0] = indeg[0] == 0;
+        for (size_t h = 0; h < q.size() && unique_path[0]; ++h) {
+            const uint32_t u = q[h];
+            for (uint32_t i = 0; i < kids[u]; ++i) {
+                const uint32_t c = t.offset(u) + i;
+                if (indeg[c] == 1 && !unique_path[c]) {
+                    unique_path[c] = 1;
+                    q.push_back(c);
+                }
+            }
+        }
+    }
+    im.term_id.assign(n, kNoId);
+    for (size_t id = 0; id < P; ++id) {
+        uint32_t node = 0;
+        for (unsigned char c : t.patterns[id]) {
+            node = t.transition(node, c);
+            if (node >= n) break;
+        }
+        if (node < n && node != 0 && t.terminal(node) && unique_path[node]) im.term_id[node] = uint32_t(id);
+    }
+
+    // ---- buckets: CSR, each sorted by (length, id) -----------------------
+    im.bucket_of.assign(n, kNoId);
+    im.bk_start.push_back(0);
+    for (const auto& [node, ids] : t.buckets) {
+        if (node >= n) continue;
+        im.bucket_of[node] = uint32_t(im.bk_start.size() - 1);
+        std::vector<uint32_t> sorted = ids;
+        std::sort(sorted.begin(), sorted.end(), [&](uint32_t a, uint32_t b) {
+            return im.pat_len[a] != im.pat_len[b] ? im.pat_len[a] < im.pat_len[b] : a < b;
+        });
+        im.bk_ids.insert(im.bk_ids.end(), sorted.begin(), sorted.end());
+        im.bk_start.push_back(uint32_t(im.bk_ids.size()));
+    }
+    if (im.bk_ids.empty()) im.bk_ids.push_back(0);
+
+    // ---- node records ------------------------------------------------------
+    const uint32_t sigma = t.alphabet.size();
+    im.groups = sigma <= 32 ? 0 : (sigma + 63) / 64;
+    auto flags = [&](uint32_t u) {
+        return (t.terminal(u) ? kFlagTerminal : 0u) | (im.bucket_of[u] != kNoId ? kFlagBucket : 0u);
+    };
+    if (im.groups == 0) {
+        im.nodes.resize(size_t(n) * 2);
+        for (uint32_t u = 0; u < n; ++u) {
+            im.nodes[2 * size_t(u)] = t.cell(u)[0];
+            im.nodes[2 * size_t(u) + 1] = (kids[u] ? t.offset(u) : 0u) | flags(u);
+        }
+    } else {
+        im.nodes.resize(size_t(n) * im.groups * 4);
+        for (uint32_t u = 0; u < n; ++u) {
+            const uint32_t* c = t.cell(u);
+            uint32_t base = kids[u] ? t.offset(u) : 0u;
+            for (uint32_t g = 0; g < im.groups; ++g) {
+                const uint32_t w0 = 2 * g < t.words ? c[2 * g] : 0u;
+                const uint32_t w1 = 2 * g + 1 < t.words ? c[2 * g + 1] : 0u;
+                uint32_t* r = &im.nodes[(size_t(u) * im.groups + g) * 4];
+                r[0] = w0;
+                r[1] = w1;
+                r[2] = (base & kBaseMask) | flags(u);
+                r[3] = im.term_id[u];
+                base += uint32_t(__builtin_popcount(w0) + __builtin_popcount(w1));
+            }
+        }
+    }
+
+    // ---- report depths: min_emit (BFS) -------------------------------------
+    {
+        std::vector<uint32_t> depth(n, UINT32_MAX), q{0};
+        depth[0] = 0;
+        uint32_t min_term = UINT32_MAX;
+        for (size_t h = 0; h < q.size(); ++h) {
+            const uint32_t u = q[h];
+            if (u != 0 && t.terminal(u)) min_term = std::min(min_term, depth[u]);
+            for (uint32_t i = 0; i < kids[u]; ++i) {
+                const uint32_t c = t.offset(u) + i;
+                if (depth[c] == UINT32_MAX) {
+                    depth[c] = depth[u] + 1;
+                    q.push_back(c);
+                }
+            }
+        }
+        im.min_emit = min_term;
+        if (im.depth_limit && !t.buckets.empty()) im.min_emit = std::min(im.min_emit, im.depth_limit);
+    }
+
+    // ---- reach: longest root path (cyclic => unbounded), plus buckets ------
+    if (im.depth_limit) {
+        uint64_t r = im.depth_limit;
+        for (const auto& [node, ids] : t.buckets)
+            for (uint32_t id : ids) r = std::max<uint64_t>(r, im.pat_len[id]);
+        im.reach = r;
+    } else {
+        // iterative DFS post-order over the reachable graph
+        std::vector<uint64_t> longest(n, 0);
+        std::vector<uint8_t> state(n, 0); // 0 new, 1 on stack, 2 done
+        std::vector<std::pair<uint32_t, uint32_t>> st{{0u, 0u}};
+        state[0] = 1;
+        bool cyclic = false;
+        while (!st.empty() && !cyclic) {
+            auto& [u, i] = st.back();
+            if (i < kids[u]) {
+                const uint32_t c = t.offset(u) + i++;
+                if (state[c] == 1) cyclic = true;
+                else if (state[c] == 0) {
+                    state[c] = 1;
+                    st.emplace_back(c, 0u);
+                }
+            } else {
+                uint64_t best = 0;
+                for (uint32_t k = 0; k < kids[u]; ++k) best = std::max(best, 1 + longest[t.offset(u) + k]);
+                longest[u] = best;
+                state[u] = 2;
+                st.pop_back();
+            }
+        }
+        im.reach = cyclic ? UINT64_MAX : longest[0];
+    }
+
+    // ---- start filter --------------------------------------------------------
+    if (im.min_emit != UINT32_MAX) {
+        const uint32_t k = std::min(im.min_emit, kMaxFilterKey);
+        im.filter_k = k;
+        std::vector<uint64_t> grams;
+        const uint64_t cap = uint64_t(1) << 22;
+        struct Frame {
+            uint32_t node, depth;
+            uint64_t key;
+        };
+        std::vector<Frame> st{{0u, 0u, 0ull}};
+        bool overflow = false;
+        while (!st.empty() && !overflow) {
+            Frame f = st.back();
+            st.pop_back();
+            if (f.depth == k) {
+                grams.push_back(f.key);
+                overflow = grams.size() > cap;
+                continue;
+            }
+            const uint32_t* c = t.cell(f.node);
+            uint32_t child = t.offset(f.node);
+            for (uint32_t w = 0; w < t.words; ++w)
+                for (uint32_t bits = c[w]; bits; bits &= bits - 1) {
+                    const uint32_t s = w * 32 + uint32_t(__builtin_ctz(bits));
+                    const uint64_t b = t.alphabet.byte_of(s);
+                    st.push_back({child++, f.depth + 1, f.key | (b << (8 * f.depth))});
+                }
+        }
+        im.filter_paths = grams.size();
+        if (grams.empty()) {
+            im.min_emit = UINT32_MAX; // no start can reach a reporting depth
+        } else if (!overflow) {
+            const uint32_t bits =
+                std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, opt.max_filter_bits);
+            im.filter_bits = bits;
+            im.filter.assign((size_t(1) << bits) / 32, 0u);
+            for (uint64_t g : grams) {
+                const uint32_t s = k <= 4 ? filter_slot32(uint32_t(g), bits) : filter_slot64(g, bits);
+                im.filter[s >> 5] |= 1u << (s & 31);
+            }
+        }
+    }
+    if (im.filter.empty()) im.filter.push_back(0);
+
+    for (uint32_t u = 0; u < n; ++u)
+        if (t.terminal(u) && u != 0) (im.term_id[u] == kNoId ? im.keyed_terminals : im.private_terminals)++;
+    return im;
+}
+
+} // namespace hfb

@@ -1,0 +1,50 @@
+// image.hpp -- host-side builder of the GPU trie image (north-star subsystem
+// 1: "the trie compiler still runs on the host but emits a GPU layout").
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "../cuda/layout.hpp"
+#include "core.hpp"
+
+namespace hfb {
+
+struct GpuImage {
+    uint32_t node_count = 0;
+    uint32_t groups = 0; // 0 = narrow uint2 records, else uint4 records per node
+    std::vector<uint32_t> nodes;
+    std::vector<uint32_t> term_id, bucket_of;
+    bool identity = false;
+    std::array<uint16_t, 256> symtab{};
+    uint32_t depth_limit = 0;
+
+    std::vector<uint8_t> pat_bytes;
+    std::vector<uint64_t> pat_off;
+    std::vector<uint32_t> pat_len;
+    std::vector<uint64_t> ht_key;
+    std::vector<uint32_t> ht_id;
+    uint64_t ht_mask = 0, hmul = 0;
+
+    std::vector<uint32_t> bk_start, bk_ids;
+
+    uint32_t filter_k = 0, filter_bits = 0;
+    uint64_t filter_paths = 0;
+    std::vector<uint32_t> filter;
+
+    uint32_t min_emit = UINT32_MAX; // shortest depth at which any start can report
+    uint64_t reach = 0;             // max bytes one start may read; UINT64_MAX = unbounded
+    uint64_t private_terminals = 0, keyed_terminals = 0;
+
+    size_t device_bytes() const;
+};
+
+struct ImageOptions {
+    uint32_t max_filter_bits = 18; // bitmap of 2^bits bits kept in shared memory
+    uint32_t filter_slack = 5;     // bits above log2(#k-grams): density <= 2^-slack
+};
+
+ImageOptions image_options_from_env();
+GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt);
+
+} // namespace hfb

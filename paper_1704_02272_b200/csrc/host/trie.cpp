@@ -1,0 +1,450 @@
+// trie.cpp -- the host trie compiler: canonical bitmap trie, compression
+// stages and prefix truncation.
+//
+// The canonical layout is an API-visible artefact (node indices come back
+// from hepfac_trie_transition, node counts and .htri bytes are compared by
+// callers), so its placement rules follow the reference exactly:
+//   - node = ceil(sigma/32) bitmap words + offset word (MSB terminal)
+//     (reference trie.hpp:45-59);
+//   - breadth-first, first-reference placement; a multi-child run is
+//     consecutive and an already-placed node inside a run gets a shallow copy
+//     slot (trie.cpp:133-217);
+//   - stage 1 / stage 2 / truncation rewrite rules (compression.cpp:58-176,
+//     prefix.cpp:14-51).
+// The construction itself is different: stage-0 tries are built level by
+// level from the symbol-sorted pattern list (no pointer graph, no queue),
+// and rewrites operate on a flat CSR graph.
+#include <algorithm>
+#include <numeric>
+#include <unordered_map>
+
+#include "core.hpp"
+
+namespace hfb {
+
+std::string format_mib(uint64_t bytes)
+{
+    uint64_t tenths = (bytes * 10) >> 20; // truncated, not rounded
+    return std::to_string(tenths / 10) + "." + std::to_string(tenths % 10);
+}
+
+double reduction_percent(uint64_t before, uint64_t after)
+{
+    return after == 0 ? 0.0 : 100.0 * double(before - after) / double(after);
+}
+
+uint32_t Trie::child_count(uint32_t n) const
+{
+    const uint32_t* c = cell(n);
+    uint32_t k = 0;
+    for (uint32_t i = 0; i < words; ++i) k += uint32_t(__builtin_popcount(c[i]));
+    return k;
+}
+
+uint32_t Trie::transition(uint32_t node, uint8_t byte) const
+{
+    int s = alphabet.symbol_of(byte);
+    if (s < 0) return kNone;
+    const uint32_t* c = cell(node);
+    const uint32_t w = uint32_t(s) >> 5, bit = 1u << (uint32_t(s) & 31u);
+    if (!(c[w] & bit)) return kNone;
+    uint32_t rank = uint32_t(__builtin_popcount(c[w] & (bit - 1)));
+    for (uint32_t i = 0; i < w; ++i) rank += uint32_t(__builtin_popcount(c[i]));
+    return (c[words] & kOffsetMask) + rank;
+}
+
+void Trie::set_lengths()
+{
+    min_len = max_len = 0;
+    for (const auto& p : patterns) {
+        uint32_t l = uint32_t(p.size());
+        if (min_len == 0 || l < min_len) min_len = l;
+        max_len = std::max(max_len, l);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage-0 construction.
+//
+// In a tree laid out breadth-first with children in symbol order, the nodes of
+// depth d appear in lexicographic (symbol-wise) order of the prefixes they
+// spell.  So sorting the patterns once and sweeping depth by depth numbers
+// every node directly: a new node starts wherever (parent, symbol) changes
+// along the sorted list.
+std::unique_ptr<Trie> build_trie(const PatternSet& set)
+{
+    if (set.patterns.empty()) invalid("empty pattern set");
+    for (const auto& p : set.patterns)
+        if (p.size() > 65535) invalid("pattern longer than 65535 bytes");
+
+    const Alphabet& a = set.alphabet;
+    const size_t n = set.patterns.size();
+    std::vector<std::string> keys(n); // symbol-index strings: byte order == symbol order
+    for (size_t i = 0; i < n; ++i) {
+        const std::string& p = set.patterns[i];
+        keys[i].resize(p.size());
+        for (size_t j = 0; j < p.size(); ++j) keys[i][j] = char(a.symbol_of(uint8_t(p[j])));
+    }
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return keys[x] < keys[y]; });
+
+    auto t = std::make_unique<Trie>(a);
+    const uint32_t stride = t->stride();
+    std::vector<uint32_t>& cells = t->cells;
+    cells.assign(stride, 0); // root
+    uint64_t nodes = 1;
+
+    std::vector<uint32_t> active(order); // patterns still longer than the current depth
+    std::vector<uint32_t> at(n, 0);      // node currently reached by each pattern
+    std::vector<uint32_t> next_active;
+    for (uint32_t depth = 0; !active.empty(); ++depth) {
+        next_active.clear();
+        uint32_t last_parent = Trie::kNone, last_sym = Trie::kNone, last_node = 0;
+        for (uint32_t i : active) {
+            const uint32_t parent = at[i];
+            const uint32_t sym = uint8_t(keys[i][depth]);
+            if (parent != last_parent || sym != last_sym) {
+                if (nodes >= Trie::kMaxNodes) invalid("trie too large");
+                last_node = uint32_t(nodes++);
+                cells.resize(size_t(nodes) * stride, 0);
+                uint32_t* pc = cells.data() + size_t(parent) * stride;
+                bool first_child = true;
+                for (uint32_t w = 0; w < t->words; ++w) first_child = first_child && pc[w] == 0;
+                if (first_child) pc[t->words] = (pc[t->words] & Trie::kTerminal) | last_node;
+                pc[sym >> 5] |= 1u << (sym & 31u);
+                last_parent = parent;
+                last_sym = sym;
+            }
+            at[i] = last_node;
+            if (keys[i].size() == depth + 1)
+                cells[size_t(last_node) * stride + t->words] |= Trie::kTerminal;
+            else
+                next_active.push_back(i);
+        }
+        active.swap(next_active);
+    }
+    t->node_count = uint32_t(nodes);
+    t->patterns = set.patterns;
+    t->set_lengths();
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Flat graph form used by the rewrite passes.  Node ids are the source trie's
+// array indices; each node owns a contiguous edge range (symbol ascending).
+
+namespace {
+
+struct Graph {
+    std::vector<uint32_t> first, degree; // edge range per node
+    std::vector<uint16_t> sym;
+    std::vector<uint32_t> dst;
+    std::vector<uint8_t> term;
+
+    uint32_t size() const { return uint32_t(first.size()); }
+    uint32_t only_child(uint32_t u) const { return dst[first[u]]; }
+};
+
+Graph graph_of(const Trie& t)
+{
+    Graph g;
+    const uint32_t n = t.node_count;
+    g.first.resize(n);
+    g.degree.resize(n);
+    g.term.resize(n);
+    size_t edges = 0;
+    for (uint32_t u = 0; u < n; ++u) edges += t.child_count(u);
+    g.sym.reserve(edges);
+    g.dst.reserve(edges);
+    for (uint32_t u = 0; u < n; ++u) {
+        const uint32_t* c = t.cell(u);
+        g.first[u] = uint32_t(g.dst.size());
+        g.term[u] = (c[t.words] & Trie::kTerminal) ? 1 : 0;
+        uint32_t target = c[t.words] & Trie::kOffsetMask;
+        for (uint32_t w = 0; w < t.words; ++w) {
+            uint32_t bits = c[w];
+            while (bits) {
+                uint32_t b = uint32_t(__builtin_ctz(bits));
+                bits &= bits - 1;
+                g.sym.push_back(uint16_t(w * 32 + b));
+                g.dst.push_back(target++);
+            }
+        }
+        g.degree[u] = uint32_t(g.dst.size()) - g.first[u];
+    }
+    return g;
+}
+
+// Breadth-first first-reference emission (the reference's TrieAssembler rule).
+// `bucket_src` (optional) maps source node -> pattern ids; keys are remapped to
+// the emitted primary slots.
+std::unique_ptr<Trie> emit(const Graph& g, const Trie& like, Stage stage,
+                           std::optional<uint32_t> depth_limit,
+                           const std::vector<std::pair<uint32_t, std::vector<uint32_t>>>* bucket_src)
+{
+    constexpr uint32_t kUnplaced = Trie::kNone;
+    std::vector<uint32_t> slot_of_node(g.size(), kUnplaced); // primary slot per graph node
+    std::vector<uint32_t> node_of_slot;
+    std::vector<uint8_t> copy_slot;
+    std::vector<uint32_t> child_base;
+
+    auto new_slot = [&](uint32_t u, bool copy) {
+        uint32_t s = uint32_t(node_of_slot.size());
+        if (s >= Trie::kMaxNodes) fail(HEPFAC_ERR_INTERNAL, "trie exceeds 2^31-1 nodes");
+        node_of_slot.push_back(u);
+        copy_slot.push_back(copy ? 1 : 0);
+        child_base.push_back(0);
+        if (!copy) slot_of_node[u] = s;
+        return s;
+    };
+
+    new_slot(0, false);
+    for (size_t head = 0; head < node_of_slot.size(); ++head) {
+        if (copy_slot[head]) continue; // copies are never expanded
+        const uint32_t u = node_of_slot[head];
+        const uint32_t deg = g.degree[u];
+        if (deg == 0) continue;
+        if (deg == 1) {
+            const uint32_t c = g.only_child(u);
+            if (slot_of_node[c] == kUnplaced) new_slot(c, false);
+            child_base[head] = slot_of_node[c];
+            continue;
+        }
+        const uint32_t run = uint32_t(node_of_slot.size());
+        for (uint32_t e = g.first[u]; e < g.first[u] + deg; ++e) {
+            const uint32_t c = g.dst[e];
+            new_slot(c, slot_of_node[c] != kUnplaced);
+        }
+        child_base[head] = run;
+    }
+    // Note: primary slots are appended in discovery order and the loop above
+    // visits them in that same order, which is exactly a FIFO queue of
+    // primaries (copies are skipped).
+
+    auto t = std::make_unique<Trie>(like.alphabet);
+    t->node_count = uint32_t(node_of_slot.size());
+    const uint32_t stride = t->stride();
+    t->cells.assign(size_t(t->node_count) * stride, 0);
+    for (uint32_t s = 0; s < t->node_count; ++s) {
+        const uint32_t u = node_of_slot[s];
+        uint32_t* c = t->cells.data() + size_t(s) * stride;
+        for (uint32_t e = g.first[u]; e < g.first[u] + g.degree[u]; ++e)
+            c[g.sym[e] >> 5] |= 1u << (g.sym[e] & 31u);
+        const uint32_t src = copy_slot[s] ? slot_of_node[u] : s;
+        c[t->words] = (child_base[src] & Trie::kOffsetMask) | (g.term[u] ? Trie::kTerminal : 0u);
+    }
+    t->patterns = like.patterns;
+    t->set_lengths();
+    t->stage = stage;
+    t->depth_limit = depth_limit;
+    if (bucket_src) {
+        for (const auto& [u, ids] : *bucket_src) {
+            if (slot_of_node[u] == kUnplaced) continue;
+            auto sorted = ids;
+            std::sort(sorted.begin(), sorted.end());
+            t->buckets.emplace_back(slot_of_node[u], std::move(sorted));
+        }
+        std::sort(t->buckets.begin(), t->buckets.end(),
+                  [](const auto& x, const auto& y) { return x.first < y.first; });
+    }
+    return t;
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// Stage 1 (reference compression.cpp:58-94): every childless terminal below a
+// unary parent is redirected to one shared terminal, the lowest-indexed
+// childless terminal.  Multi-child parents keep private leaves because two
+// slots of one run cannot alias a single cell (compression.hpp:26-31).
+std::unique_ptr<Trie> merge_final_nodes(const Trie& t, CompressionStats* stats)
+{
+    if (t.stage != Stage::None) fail(HEPFAC_ERR_STATE, "trie is already compressed");
+    if (t.depth_limit) invalid("cannot compress a truncated trie");
+    Graph g = graph_of(t);
+    uint32_t shared = Trie::kNone;
+    for (uint32_t u = 0; u < g.size() && shared == Trie::kNone; ++u)
+        if (g.term[u] && g.degree[u] == 0) shared = u;
+    if (shared != Trie::kNone)
+        for (uint32_t u = 0; u < g.size(); ++u) {
+            if (g.degree[u] != 1) continue;
+            uint32_t& c = g.dst[g.first[u]];
+            if (g.term[c] && g.degree[c] == 0) c = shared;
+        }
+    auto out = emit(g, t, Stage::FinalMerged, std::nullopt, nullptr);
+    if (stats) {
+        stats->nodes_before = t.node_count;
+        stats->nodes_after_stage1 = stats->nodes_after_stage2 = out->node_count;
+        stats->pattern_count = t.patterns.size();
+        stats->reduction_percent = reduction_percent(t.node_count, out->node_count);
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2 (reference compression.cpp:96-176): tails of up to three unary,
+// non-terminal nodes ending in a shared terminal are merged into one class
+// representative per suffix string.
+std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
+{
+    if (t.stage != Stage::FinalMerged) fail(HEPFAC_ERR_STATE, "tail merge requires stage-1 output");
+    Graph g = graph_of(t);
+    const Alphabet& a = t.alphabet;
+
+    auto child_by_sym = [&](uint32_t u, uint32_t s) {
+        for (uint32_t e = g.first[u]; e < g.first[u] + g.degree[u]; ++e)
+            if (g.sym[e] == s) return g.dst[e];
+        return Trie::kNone;
+    };
+    auto leaf_terminal = [&](uint32_t u) { return g.term[u] && g.degree[u] == 0; };
+    // A suffix of k <= 3 raw bytes, tagged with k, packed into 32 bits.
+    auto suffix_key = [](const std::string& p, uint32_t k) {
+        uint32_t key = k << 24;
+        for (uint32_t i = 0; i < k; ++i) key |= uint32_t(uint8_t(p[p.size() - k + i])) << (8 * (2 - i));
+        return key;
+    };
+
+    std::unordered_map<uint32_t, uint32_t> rep_of_suffix; // suffix -> representative node
+    std::vector<std::pair<uint32_t, uint32_t>> reps;      // (node, suffix) in creation order
+    std::vector<std::pair<uint32_t, uint32_t>> rewires;   // (parent, new only child)
+    std::vector<uint32_t> path;
+
+    for (const auto& p : t.patterns) {
+        const uint32_t L = uint32_t(p.size());
+        if (L < 4) continue;
+        path.assign(1, 0u);
+        for (unsigned char ch : p) {
+            uint32_t nx = child_by_sym(path.back(), uint32_t(a.symbol_of(ch)));
+            if (nx == Trie::kNone) fail(HEPFAC_ERR_INTERNAL, "pattern missing from trie");
+            path.push_back(nx);
+        }
+        // Longest eligible chain: path[L-k] unary & non-terminal, the deepest one
+        // pointing at a shared (leaf) terminal.
+        uint32_t chain = 0;
+        for (uint32_t k = 1; k <= 3; ++k) {
+            const uint32_t v = path[L - k];
+            if (g.term[v] || g.degree[v] != 1) break;
+            if (k == 1 && !leaf_terminal(g.only_child(v))) break;
+            chain = k;
+        }
+        // The edge into the chain head must belong to a unary parent.
+        while (chain >= 1 && g.degree[path[L - chain - 1]] > 1) --chain;
+        if (chain == 0) continue;
+
+        uint32_t replace = 0; // deepest level whose class already has another owner
+        for (uint32_t k = chain; k >= 1; --k) {
+            auto it = rep_of_suffix.find(suffix_key(p, k));
+            if (it != rep_of_suffix.end() && it->second != path[L - k]) {
+                replace = k;
+                break;
+            }
+        }
+        for (uint32_t k = replace + 1; k <= chain; ++k) {
+            const uint32_t key = suffix_key(p, k);
+            if (rep_of_suffix.emplace(key, path[L - k]).second) reps.emplace_back(path[L - k], key);
+        }
+        if (replace >= 1)
+            rewires.emplace_back(path[L - replace - 1], rep_of_suffix.at(suffix_key(p, replace)));
+    }
+
+    // Representatives of k-suffixes point at the representative of their
+    // (k-1)-suffix, then replaced chains are cut over.
+    for (const auto& [node, key] : reps) {
+        const uint32_t k = key >> 24;
+        if (k < 2) continue;
+        // drop the first byte: shift the remaining k-1 bytes up one position
+        const uint32_t sub = ((k - 1) << 24) | ((key << 8) & 0x00FFFF00u);
+        auto it = rep_of_suffix.find(sub);
+        if (it != rep_of_suffix.end()) g.dst[g.first[node]] = it->second;
+    }
+    for (const auto& [parent, child] : rewires) g.dst[g.first[parent]] = child;
+
+    auto out = emit(g, t, Stage::TailMerged, std::nullopt, nullptr);
+    if (stats) {
+        stats->nodes_before = t.node_count;
+        stats->nodes_after_stage1 = t.node_count;
+        stats->nodes_after_stage2 = out->node_count;
+        stats->pattern_count = t.patterns.size();
+        stats->reduction_percent = reduction_percent(t.node_count, out->node_count);
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Truncation (reference prefix.cpp:14-51).
+
+std::vector<uint32_t> first_reach_depths(const Trie& t)
+{
+    std::vector<uint32_t> depth(t.node_count, Trie::kNone);
+    std::vector<uint32_t> frontier{0}, next;
+    depth[0] = 0;
+    for (uint32_t d = 0; !frontier.empty(); ++d) {
+        next.clear();
+        for (uint32_t u : frontier) {
+            const uint32_t k = t.child_count(u), base = t.offset(u);
+            for (uint32_t i = 0; i < k; ++i)
+                if (depth[base + i] == Trie::kNone) {
+                    depth[base + i] = d + 1;
+                    next.push_back(base + i);
+                }
+        }
+        frontier.swap(next);
+    }
+    return depth;
+}
+
+std::vector<std::pair<uint32_t, std::vector<uint32_t>>> verification_buckets(const Trie& t,
+                                                                              uint32_t depth)
+{
+    std::unordered_map<uint32_t, std::vector<uint32_t>> by_node;
+    for (uint32_t id = 0; id < t.patterns.size(); ++id) {
+        const std::string& p = t.patterns[id];
+        if (p.size() <= depth) continue;
+        uint32_t node = 0;
+        for (uint32_t i = 0; i < depth; ++i) {
+            node = t.transition(node, uint8_t(p[i]));
+            if (node >= t.node_count) fail(HEPFAC_ERR_INTERNAL, "dictionary pattern not present in trie");
+        }
+        by_node[node].push_back(id); // ids arrive ascending
+    }
+    std::vector<std::pair<uint32_t, std::vector<uint32_t>>> out(by_node.begin(), by_node.end());
+    std::sort(out.begin(), out.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    return out;
+}
+
+static std::unique_ptr<Trie> clone(const Trie& t)
+{
+    auto c = std::make_unique<Trie>(t.alphabet);
+    c->node_count = t.node_count;
+    c->cells = t.cells;
+    c->patterns = t.patterns;
+    c->min_len = t.min_len;
+    c->max_len = t.max_len;
+    c->stage = t.stage;
+    c->depth_limit = t.depth_limit;
+    c->buckets = t.buckets;
+    c->loaded = t.loaded;
+    return c;
+}
+
+std::unique_ptr<Trie> truncate_trie(const Trie& t, uint32_t depth, bool* was_noop)
+{
+    if (depth == 0) invalid("truncation depth must be >= 1");
+    if (t.stage == Stage::TailMerged) fail(HEPFAC_ERR_STATE, "cannot truncate a tail-merged trie");
+    if (t.depth_limit) fail(HEPFAC_ERR_STATE, "trie is already truncated");
+    if (depth >= t.max_len) {
+        if (was_noop) *was_noop = true;
+        return clone(t);
+    }
+    Graph g = graph_of(t);
+    const auto depths = first_reach_depths(t);
+    for (uint32_t u = 0; u < g.size(); ++u)
+        if (depths[u] >= depth) g.degree[u] = 0;
+    const auto buckets = verification_buckets(t, depth);
+    auto out = emit(g, t, t.stage, depth, &buckets);
+    if (was_noop) *was_noop = false;
+    return out;
+}
+
+} // namespace hfb

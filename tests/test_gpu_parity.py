@@ -1,0 +1,231 @@
+"""GPU parity: hepfac_scan (sm_100a kernel, called through the C ABI) against
+the oracles.  Bar: bit-exact hepfac_match_t arrays.
+
+Cases follow the reference's own tests: test_capi.cpp:30-100 (end-to-end KAT),
+test_scan.cpp:19-143 (single offsets, nesting, brute-force equality, unit
+boundaries, periodic overlaps, two-stage), acceptance.cpp:101-150 (criteria 3
+and 4: random instances, all trie states, truncation depths {1,2,5,8}).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import alphabet_bytes, as_tuples, pattern_set, plant, same, text
+
+pytestmark = pytest.mark.gpu
+
+
+def build(lib, pats, sigma=256, stages=0, depth=None):
+    a = lib.alphabet(sigma)
+    t = lib.build_trie(lib.patterns(pats, a))
+    if stages:
+        t, _ = t.compress(stages)
+    if depth is not None:
+        t, noop = t.truncate(depth)
+    return t
+
+
+def test_capi_end_to_end_known_answer(gpu, tmp_path):
+    # test_capi.cpp:30-100: stage-2 trie, saved, loaded, scanned.
+    t = build(gpu, [b"ABCXYZ", b"DEFXYZ", b"AB"], stages=2)
+    path = str(tmp_path / "t.htri")
+    t.save(path)
+    loaded = gpu.load_trie(path)
+    assert loaded.node_count() == 9 and loaded.stage() == 2
+    got = gpu.scan(loaded, b"xxABCXYZ--DEFXYZ++ABq", workers=2, chunk=8)
+    assert as_tuples(got) == [(2, 2, 2), (2, 6, 0), (10, 6, 1), (18, 2, 2)]
+
+
+def test_single_offsets_and_nesting(gpu):
+    # test_scan.cpp:19-41
+    assert as_tuples(gpu.scan(build(gpu, [b"AB"]), b"XABY")) == [(1, 2, 0)]
+    assert as_tuples(gpu.scan(build(gpu, [b"AB", b"ABC"]), b"ABC")) == [(0, 2, 0), (0, 3, 1)]
+    assert gpu.scan(build(gpu, [b"ACG"]), b"xyzxyzxyz").size == 0
+
+
+def test_periodic_overlaps(gpu):
+    # test_scan.cpp:90-101
+    s = b"AB" * 50
+    hits = gpu.scan(build(gpu, [b"ABAB"]), s)
+    assert hits.size == (len(s) - 4) // 2 + 1
+    assert list(hits["start"]) == [2 * i for i in range(hits.size)]
+
+
+def test_empty_and_tiny_texts(gpu):
+    t = build(gpu, [b"ABC", b"Q"])
+    assert gpu.scan(t, b"").size == 0
+    assert as_tuples(gpu.scan(t, b"Q")) == [(0, 1, 1)]
+    assert gpu.scan(t, b"AB").size == 0
+    assert as_tuples(gpu.scan(t, b"ABC")) == [(0, 3, 0)]
+
+
+@pytest.mark.parametrize("sigma", [2, 4, 20, 52, 64, 128, 256])
+def test_random_instances_all_states(gpu, sigma):
+    # acceptance criteria 3 + 4 shape: random sets, planted + boundary copies.
+    rng = np.random.default_rng(1000 + sigma)
+    a, syms = alphabet_bytes(gpu, sigma)
+    for rep in range(6):
+        n = int(rng.integers(1, 200))
+        pats = pattern_set(rng, syms, n, 2, 20)
+        n = len(pats)
+        tl = int(rng.integers(1024, 64 * 1024))
+        tx = text(rng, syms, tl)
+        for _ in range(n // 4 + 1):
+            plant(tx, pats[int(rng.integers(0, n))], int(rng.integers(0, tl)))
+        for c in range(4096 - 7, tl, 4096):  # astride kernel tile boundaries
+            p = pats[int(rng.integers(0, n))]
+            plant(tx, p, max(0, c - len(p) // 2))
+        want = oracle.naive_find_all(tx, pats)
+        full = build(gpu, pats, sigma)
+        assert same(gpu.scan(full, tx), want), ("stage0", sigma, rep)
+        s1, _ = full.compress(1)
+        s2, _ = full.compress(2)
+        assert same(gpu.scan(s1, tx), want), ("stage1", sigma, rep)
+        assert same(gpu.scan(s2, tx), want), ("stage2", sigma, rep)
+        for d in (1, 2, 5, 8):
+            for base in (full, s1):
+                tr, noop = base.truncate(d)
+                if noop:
+                    continue
+                assert same(gpu.scan(tr, tx), want), ("trunc", d, sigma, rep)
+
+
+def test_matches_walk_oracle_and_reference(gpu, ref):
+    # Same trie bytes through three engines: GPU, C restatement, reference.
+    rng = np.random.default_rng(5)
+    a, syms = alphabet_bytes(gpu, 52)
+    pats = pattern_set(rng, syms, 80, 6, 20)
+    tx = text(rng, syms, 32768)
+    for i in range(0, len(pats), 3):
+        plant(tx, pats[i], int(rng.integers(0, 32000)))
+    t = build(gpu, pats, 52, stages=1)
+    tr, _ = t.truncate(5)
+    ra = ref.alphabet(52)
+    rt, _ = ref.build_trie(ref.patterns(pats, ra)).compress(1)
+    rtr, _ = rt.truncate(5)
+    assert tr.save_bytes() == rtr.save_bytes()
+    want = ref.scan(rtr, tx, workers=2, chunk=512)
+    assert same(oracle.walk_scan(tr.save_bytes(), tx), want)
+    assert same(gpu.scan(tr, tx), want)
+
+
+def test_long_patterns_beyond_shared_halo(gpu):
+    # walks and verifications that read past the 64-byte shared-memory halo
+    rng = np.random.default_rng(11)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = [bytes(rng.integers(0, 256, size=n, dtype=np.uint8)) for n in (70, 150, 300, 1000, 5000)]
+    pats.append(pats[0][:40])
+    tx = text(rng, syms, 50000)
+    for i, p in enumerate(pats):
+        for k in range(3):
+            plant(tx, p, 4096 * (k + 1) - 10 * i - 1)
+    want = oracle.naive_find_all(tx, pats)
+    assert want.size >= 15
+    for stages, depth in ((0, None), (1, None), (2, None), (0, 3), (1, 33)):
+        assert same(gpu.scan(build(gpu, pats, 256, stages, depth), tx), want), (stages, depth)
+
+
+def test_bytes_outside_alphabet_kill_walks(gpu):
+    pats = [b"ACGT", b"GATTACA", b"CC"]
+    tx = b"ACGTxACGTNNGATTACACCxC" * 50
+    want = oracle.naive_find_all(tx, pats)
+    for stages in (0, 1, 2):
+        assert same(gpu.scan(build(gpu, pats, 4, stages), tx), want)
+
+
+def test_permuted_byte_alphabet(gpu):
+    sym = bytes(np.random.default_rng(3).permutation(256).astype(np.uint8))
+    a = gpu.alphabet(sym)
+    rng = np.random.default_rng(4)
+    pats = pattern_set(rng, np.arange(256, dtype=np.uint8), 100, 1, 6)
+    t = gpu.build_trie(gpu.patterns(pats, a))
+    tx = rng.integers(0, 256, size=200000, dtype=np.uint8)
+    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
+
+
+def test_dense_nested_matches_overflow_capacity(gpu):
+    # every offset reports up to 32 nested patterns: forces the exact-size re-run
+    pats = [b"A" * k for k in range(1, 33)]
+    tx = b"A" * 300000
+    got = gpu.scan(build(gpu, pats, 256), tx)
+    n = len(tx)
+    assert got.size == sum(n - k + 1 for k in range(1, 33))
+    assert same(got, oracle.naive_find_all(tx, pats))
+    assert gpu.last_scan_stats()["relaunches"] in (0, 1)
+
+
+def test_text_sizes_around_tiles(gpu):
+    rng = np.random.default_rng(9)
+    syms = np.frombuffer(b"ACGT", dtype=np.uint8)
+    pats = pattern_set(rng, syms, 300, 3, 9)
+    t = build(gpu, pats, 4, 1)
+    for n in (1, 2, 3, 15, 16, 17, 4095, 4096, 4097, 8191, 8192, 8193, 4096 * 37 + 5):
+        tx = text(rng, syms, n)
+        assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats)), n
+
+
+def test_shards_concatenate_to_full_scan(gpu):
+    rng = np.random.default_rng(21)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 500, 2, 24)
+    tx = text(rng, syms, 1 << 18)
+    for i, p in enumerate(pats):
+        plant(tx, p, (i * 523) % (tx.size - 30))
+    t = build(gpu, pats, 256, 2)
+    full = gpu.scan(t, tx)
+    halo = gpu.halo(t)
+    assert halo == 23
+    N = tx.size
+    for shards in (2, 3, 8):
+        parts = []
+        for g in range(shards):
+            lo, hi = g * N // shards, (g + 1) * N // shards
+            end = min(N, hi + halo)
+            parts.append(gpu.scan_shard(t, tx[lo:end], lo, hi - lo))
+        assert same(np.concatenate(parts), full), shards
+
+
+def test_run_throughput_report(gpu):
+    rng = np.random.default_rng(2)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 1000, 4, 32)
+    tx = text(rng, syms, 1 << 22)
+    t = build(gpu, pats, 256, 2)
+    rep = gpu.run_throughput(t, tx, runs=3, workers=5)
+    assert rep["bytes"] == tx.size and rep["runs"] == 3 and rep["workers"] == 5
+    assert rep["seconds"] > 0 and rep["gbps"] > 0
+    assert rep["matches"] == gpu.scan(t, tx).size
+
+
+def test_session_device_resident(gpu):
+    rng = np.random.default_rng(8)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 2000, 4, 32)
+    tx = text(rng, syms, 1 << 21)
+    for i, p in enumerate(pats):
+        plant(tx, p, (i * 1009) % (tx.size - 40))
+    t = build(gpu, pats, 256, 2)
+    s = gpu.session(t, tx)
+    ms, m = s.run(3)
+    assert len(ms) == 3 and all(x > 0 for x in ms)
+    assert same(s.fetch(), oracle.naive_find_all(tx, pats))
+    s.close()
+
+
+def test_config1_against_reference(gpu, ref):
+    # BASELINE config 1: 1,000 byte patterns len 4-32, 16 MiB, 1 plant / 4 KiB.
+    rng = np.random.default_rng(20240601)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 1000, 4, 32)
+    tx = text(rng, syms, 16 << 20)
+    for i in range(4096):
+        p = pats[i % len(pats)]
+        plant(tx, p, int(rng.integers(0, tx.size - len(p))))
+    ra = ref.alphabet(256)
+    rt, _ = ref.build_trie(ref.patterns(pats, ra)).compress(2)
+    want = ref.scan(rt, tx, workers=os.cpu_count() or 1)
+    t = build(gpu, pats, 256, 2)
+    assert same(gpu.scan(t, tx), want)
+    assert want.size >= 4096
