@@ -48,10 +48,13 @@ typedef struct hepfac_b200_scan_stats {
 
 hepfac_status_t hepfac_b200_last_scan_stats(hepfac_b200_scan_stats_t* out);
 
-/* Device-resident session: text uploaded once, scanned repeatedly. */
+/* Device-resident session: text uploaded once, scanned repeatedly.  Same
+ * shard convention as hepfac_b200_scan_shard (offset = 0, owned = bytes for a
+ * whole text). */
 typedef struct hepfac_b200_session hepfac_b200_session_t;
 hepfac_status_t hepfac_b200_session_create(const hepfac_trie_t* trie, const uint8_t* text,
-                                           uint64_t bytes, hepfac_b200_session_t** out);
+                                           uint64_t bytes, uint64_t offset, uint64_t owned,
+                                           hepfac_b200_session_t** out);
 /* Runs `iterations` scans; ms_each[i] (may be NULL) = device time of scan i.
  * flush_l2 != 0 evicts L2 before each (untimed). */
 hepfac_status_t hepfac_b200_session_run(hepfac_b200_session_t* session, uint32_t iterations,

@@ -535,7 +535,7 @@ Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes
 struct Session {
     std::shared_ptr<DeviceTrie> dt;
     std::unique_ptr<Workspace> ws;
-    uint64_t bytes = 0, matches = 0;
+    uint64_t bytes = 0, matches = 0, offset = 0, owned = 0;
     std::vector<cudaEvent_t> evs;
     ~Session()
     {
@@ -545,15 +545,18 @@ struct Session {
     }
 };
 
-Session* session_create(const Trie& t, const uint8_t* text, uint64_t bytes)
+Session* session_create(const Trie& t, const uint8_t* text, uint64_t bytes, uint64_t offset, uint64_t owned)
 {
     if (bytes == 0) invalid("empty corpus");
+    if (owned > bytes) invalid("shard owns more starts than it has bytes");
     const int dev = pick_device();
     DeviceGuard g(dev);
     auto s = std::make_unique<Session>();
     s->dt = t.device_image(dev);
     s->ws = std::make_unique<Workspace>(dev);
     s->bytes = bytes;
+    s->offset = offset;
+    s->owned = owned;
     s->ws->ensure_text(bytes);
     CK(cudaMemcpy(s->ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
     s->ws->ensure_out(initial_capacity(bytes));
@@ -582,7 +585,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         if (flush_l2)
             gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
         CK(cudaEventRecord(s->evs[2 * i], ws.stream));
-        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->bytes, s->bytes, 0, ws.d_out, ws.out_cap);
+        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset, ws.d_out, ws.out_cap);
         CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
     }
     fetch_small(ws);

@@ -55,7 +55,7 @@ const ScanStats& last_scan_stats();
 
 // Device-resident benchmark session (hepfac_b200.h).
 struct Session;
-Session* session_create(const Trie& t, const uint8_t* host_text, uint64_t bytes);
+Session* session_create(const Trie& t, const uint8_t* host_text, uint64_t bytes, uint64_t offset, uint64_t owned);
 void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each);
 uint64_t session_matches(Session* s);
 std::unique_ptr<MatchList> session_fetch(Session* s);

@@ -158,7 +158,7 @@ _B200_PROTOTYPES = [
     ("hepfac_b200_halo", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("hepfac_b200_scan_shard", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.c_uint64, _PP]),
     ("hepfac_b200_last_scan_stats", C.c_int, [C.POINTER(_ScanStats)]),
-    ("hepfac_b200_session_create", C.c_int, [_P, _P, C.c_uint64, _PP]),
+    ("hepfac_b200_session_create", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.c_uint64, _PP]),
     ("hepfac_b200_session_run", C.c_int, [_P, C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_uint64)]),
     ("hepfac_b200_session_fetch", C.c_int, [_P, _PP]),
@@ -327,8 +327,8 @@ class Library:
         self.check(self.dll.hepfac_b200_layout_info(trie.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in _LayoutInfo._fields_}
 
-    def session(self, trie: "Trie", text) -> "Session":
-        return Session(self, trie, text)
+    def session(self, trie: "Trie", text, offset: int = 0, owned: Optional[int] = None) -> "Session":
+        return Session(self, trie, text, offset, owned)
 
 
 class Alphabet:
@@ -480,12 +480,13 @@ class Trie:
 class Session:
     """Device-resident benchmark session (hepfac_b200_session_*)."""
 
-    def __init__(self, lib: Library, trie: Trie, text):
+    def __init__(self, lib: Library, trie: Trie, text, offset: int = 0, owned: Optional[int] = None):
         self.lib, self.trie = lib, trie
         arr = _as_u8(text)
         self.h = C.c_void_p()
-        lib.check(lib.dll.hepfac_b200_session_create(trie.h, _ptr(arr), arr.size, C.byref(self.h)))
-        self.bytes = arr.size
+        owned = arr.size if owned is None else owned
+        lib.check(lib.dll.hepfac_b200_session_create(trie.h, _ptr(arr), arr.size, offset, owned, C.byref(self.h)))
+        self.bytes, self.owned = arr.size, owned
 
     def run(self, iterations: int, flush_l2: bool = False):
         ms = (C.c_double * max(1, iterations))()

@@ -117,10 +117,10 @@ def test_long_patterns_beyond_shared_halo(gpu):
     syms = np.arange(256, dtype=np.uint8)
     pats = [bytes(rng.integers(0, 256, size=n, dtype=np.uint8)) for n in (70, 150, 300, 1000, 5000)]
     pats.append(pats[0][:40])
-    tx = text(rng, syms, 50000)
+    tx = text(rng, syms, 200000)
     for i, p in enumerate(pats):
         for k in range(3):
-            plant(tx, p, 4096 * (k + 1) - 10 * i - 1)
+            plant(tx, p, 30000 * i + 9000 * k + 4095 - 17 * i)
     want = oracle.naive_find_all(tx, pats)
     assert want.size >= 15
     for stages, depth in ((0, None), (1, None), (2, None), (0, 3), (1, 33)):
