@@ -188,10 +188,12 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_words = d->kw ? uint32_t(im.filter.size()) : 0u;
     v.filter_bits = im.filter_bits;
     v.filter_k = im.filter_k;
+    v.filter_hashes = im.filter_hashes;
     v.min_emit = im.min_emit;
 
     d->kernel = select_kernel(d->grouped, d->identity, d->kw);
-    d->smem = size_t(v.filter_words) * 4 + (d->identity ? 0 : 512) + gpu::kSmemText;
+    d->smem = gpu::SmemLayout::text_bytes() + gpu::SmemLayout::queue_bytes() + size_t(v.filter_words) * 4 +
+              (d->identity ? 0 : 512);
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
@@ -222,14 +224,19 @@ struct Workspace {
     cudaEvent_t ev[4] = {};
     uint8_t* d_text = nullptr;
     size_t text_cap = 0;
-    hepfac_match_t* d_out = nullptr;
+    hepfac_match_t* d_out = nullptr;   // final, ordered records
+    hepfac_match_t* d_stage = nullptr; // per-tile slices in completion order
     uint64_t out_cap = 0;
-    unsigned long long* d_status = nullptr;
-    uint64_t status_cap = 0;
-    unsigned long long* d_small = nullptr; // [0] tile counter, [1] total, [2] error word
+    uint32_t* d_tile_count = nullptr;
+    unsigned long long* d_tile_slot = nullptr;
+    unsigned long long* d_tile_first = nullptr;
+    uint64_t tile_cap = 0;
+    unsigned long long* d_chunk = nullptr; // one per CTA of the grid
+    uint64_t chunk_cap = 0;
+    // [0] tile counter, [1] total, [2] error word, [3] staging cursor
+    unsigned long long* d_small = nullptr;
     unsigned long long* h_small = nullptr; // pinned mirror of [1], [2]
     unsigned long long ctr_base = 0;
-    uint32_t epoch = 0;
     uint4* d_flush = nullptr;
     size_t flush_n16 = 0;
 
@@ -245,47 +252,49 @@ struct Workspace {
     {
         cudaSetDevice(device);
         cudaStreamSynchronize(stream);
-        cudaFree(d_text);
-        cudaFree(d_out);
-        cudaFree(d_status);
-        cudaFree(d_small);
-        cudaFree(d_flush);
+        for (void* p : {(void*)d_text, (void*)d_out, (void*)d_stage, (void*)d_tile_count, (void*)d_tile_slot,
+                        (void*)d_tile_first, (void*)d_chunk, (void*)d_small, (void*)d_flush})
+            cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
         cudaStreamDestroy(stream);
     }
 
+    template <typename T>
+    void regrow(T*& p, uint64_t& cap, uint64_t n)
+    {
+        if (n <= cap) return;
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        p = dev_alloc<T>(size_t(n));
+        cap = n;
+    }
     void ensure_text(size_t bytes)
     {
-        const size_t need = ((bytes + 15) & ~size_t(15)) + 16;
-        if (need <= text_cap) return;
-        cudaFree(d_text);
-        d_text = nullptr;
-        text_cap = 0;
-        d_text = dev_alloc<uint8_t>(need);
-        text_cap = need;
+        uint64_t cap = text_cap;
+        regrow(d_text, cap, ((bytes + 15) & ~size_t(15)) + 16);
+        text_cap = size_t(cap);
     }
     void ensure_out(uint64_t n)
     {
         if (n <= out_cap) return;
-        CK(cudaStreamSynchronize(stream));
-        cudaFree(d_out);
-        d_out = nullptr;
-        out_cap = 0;
-        d_out = dev_alloc<hepfac_match_t>(size_t(n));
+        uint64_t c1 = out_cap, c2 = out_cap;
+        regrow(d_out, c1, n);
+        regrow(d_stage, c2, n);
         out_cap = n;
     }
-    void ensure_status(uint64_t tiles)
+    void ensure_tiles(uint64_t tiles, uint64_t grid)
     {
-        if (tiles <= status_cap) return;
-        CK(cudaStreamSynchronize(stream));
-        cudaFree(d_status);
-        d_status = nullptr;
-        status_cap = 0;
-        d_status = dev_alloc<unsigned long long>(size_t(tiles));
-        CK(cudaMemset(d_status, 0, size_t(tiles) * sizeof(unsigned long long)));
-        status_cap = tiles;
-        epoch = 0;
+        if (tiles > tile_cap) {
+            uint64_t a = tile_cap, b = tile_cap, c = tile_cap;
+            regrow(d_tile_count, a, tiles);
+            regrow(d_tile_slot, b, tiles);
+            regrow(d_tile_first, c, tiles);
+            tile_cap = tiles;
+        }
+        regrow(d_chunk, chunk_cap, grid);
     }
 };
 
@@ -322,46 +331,49 @@ struct WorkspaceLease {
 
 thread_local ScanStats t_stats;
 
-// Enqueue one kernel launch over device-resident text.  The tile counter is
-// never reset: each launch consumes exactly n_tiles + grid increments.
+// Enqueue one cooperative launch over device-resident text.  The tile
+// counter is never reset: each launch consumes exactly n_tiles + 3 * grid
+// increments (see pfac_scan_kernel).
 uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text, uint64_t n_own,
-                      uint64_t n_avail, uint64_t g0, hepfac_match_t* d_out, uint64_t cap)
+                      uint64_t n_avail, uint64_t g0)
 {
     const uint64_t n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
     if (n_tiles == 0) {
         CK(cudaMemsetAsync(ws.d_small + 1, 0, sizeof(unsigned long long), ws.stream));
         return 0;
     }
-    ws.ensure_status(n_tiles);
-    if (++ws.epoch == 0x10000u) {
-        CK(cudaMemsetAsync(ws.d_status, 0, size_t(ws.status_cap) * sizeof(unsigned long long), ws.stream));
-        ws.epoch = 1;
-    }
     const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(dt.sm_count) * dt.blocks_per_sm);
+    ws.ensure_tiles(n_tiles, grid);
     gpu::ScanArgs a{};
     a.trie = dt.view;
     a.text = d_text;
     a.n_own = n_own;
     a.n_avail = n_avail;
     a.g0 = g0;
-    a.out = d_out;
-    a.out_cap = cap;
-    a.status = ws.d_status;
+    a.out = ws.d_out;
+    a.stage = ws.d_stage;
+    a.cap = ws.out_cap;
     a.tile_ctr = ws.d_small;
     a.tile_base = ws.ctr_base;
     a.n_tiles = n_tiles;
-    a.epoch_bits = (unsigned long long)ws.epoch << 48;
+    a.tile_count = ws.d_tile_count;
+    a.tile_slot = ws.d_tile_slot;
+    a.tile_first = ws.d_tile_first;
+    a.chunk_sum = ws.d_chunk;
+    a.stage_cursor = ws.d_small + 3;
     a.total = ws.d_small + 1;
     a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
-    dt.kernel<<<unsigned(grid), gpu::kThreads, dt.smem, ws.stream>>>(a);
-    const cudaError_t e = cudaGetLastError();
+    void* params[] = {&a};
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(grid)),
+                                                      dim3(gpu::kThreads), params, dt.smem, ws.stream);
     if (e != cudaSuccess) {
+        cudaGetLastError();
         // the counter state is unknown after a failed launch: reset it
-        cudaMemset(ws.d_small, 0, sizeof(unsigned long long));
+        cudaMemset(ws.d_small, 0, 4 * sizeof(unsigned long long));
         ws.ctr_base = 0;
         cuda_fail(e, "pfac_scan_kernel launch");
     }
-    ws.ctr_base += n_tiles + grid;
+    ws.ctr_base += n_tiles + 3 * grid;
     return 1;
 }
 
@@ -411,14 +423,14 @@ std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uin
     CK(cudaEventRecord(ws->ev[0], ws->stream));
     CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
     CK(cudaEventRecord(ws->ev[1], ws->stream));
-    st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0, ws->d_out, ws->out_cap);
+    st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0);
     CK(cudaEventRecord(ws->ev[2], ws->stream));
     fetch_small(*ws);
     uint64_t total = ws->h_small[0];
     if (total > ws->out_cap) { // overflow: re-run with the exact size
         ws->ensure_out(total);
         CK(cudaEventRecord(ws->ev[1], ws->stream));
-        st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0, ws->d_out, ws->out_cap);
+        st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0);
         CK(cudaEventRecord(ws->ev[2], ws->stream));
         fetch_small(*ws);
         total = ws->h_small[0];
@@ -503,14 +515,14 @@ Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes
     if (dt->min_emit == UINT32_MAX || bytes < dt->min_emit) return r;
     ws->ensure_out(std::max(ws->out_cap, initial_capacity(bytes)));
     CK(cudaMemsetAsync(ws->d_small + 2, 0, sizeof(unsigned long long), ws->stream));
-    enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0, ws->d_out, ws->out_cap); // warm-up, untimed
+    enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0); // warm-up, untimed
     fetch_small(*ws);
     ws->ensure_out(ws->h_small[0]);
     std::vector<hepfac_match_t> host;
     double sum_scan = 0, sum_merge = 0;
     for (uint32_t i = 0; i < runs; ++i) {
         CK(cudaEventRecord(ws->ev[0], ws->stream));
-        enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0, ws->d_out, ws->out_cap);
+        enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0);
         CK(cudaEventRecord(ws->ev[1], ws->stream));
         fetch_small(*ws);
         r.matches = ws->h_small[0];
@@ -585,7 +597,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         if (flush_l2)
             gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
         CK(cudaEventRecord(s->evs[2 * i], ws.stream));
-        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset, ws.d_out, ws.out_cap);
+        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset);
         CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
     }
     fetch_small(ws);

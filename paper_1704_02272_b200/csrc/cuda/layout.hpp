@@ -52,6 +52,12 @@ HFB_HD uint32_t filter_slot64(uint64_t key, uint32_t bits)
 {
     return uint32_t((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
 }
+// Second, independent probe (Bloom filter with two hash functions).
+HFB_HD uint32_t filter_slot32b(uint32_t key, uint32_t bits) { return ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - bits); }
+HFB_HD uint32_t filter_slot64b(uint64_t key, uint32_t bits)
+{
+    return uint32_t(((key ^ (key >> 29)) * 0xBF58476D1CE4E5B9ull) >> (64 - bits));
+}
 
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {
@@ -74,6 +80,7 @@ struct TrieView {
     uint32_t filter_words;
     uint32_t filter_bits; // 0 = filter disabled (every start walks)
     uint32_t filter_k;
+    uint32_t filter_hashes; // 1 or 2 probes
     uint32_t min_emit;
 };
 

@@ -40,6 +40,10 @@ ImageOptions image_options_from_env()
         long v = std::strtol(s, nullptr, 10);
         if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
     }
+    if (const char* s = std::getenv("HEPFAC_FILTER_HASHES")) {
+        long v = std::strtol(s, nullptr, 10);
+        if (v == 1 || v == 2) o.filter_hashes = uint32_t(v);
+    }
     return o;
 }
 
@@ -277,10 +281,15 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             const uint32_t bits =
                 std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, opt.max_filter_bits);
             im.filter_bits = bits;
+            im.filter_hashes = opt.filter_hashes;
             im.filter.assign((size_t(1) << bits) / 32, 0u);
             for (uint64_t g : grams) {
                 const uint32_t s = k <= 4 ? filter_slot32(uint32_t(g), bits) : filter_slot64(g, bits);
                 im.filter[s >> 5] |= 1u << (s & 31);
+                if (im.filter_hashes > 1) {
+                    const uint32_t s2 = k <= 4 ? filter_slot32b(uint32_t(g), bits) : filter_slot64b(g, bits);
+                    im.filter[s2 >> 5] |= 1u << (s2 & 31);
+                }
             }
         }
     }

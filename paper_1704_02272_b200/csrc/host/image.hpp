@@ -28,7 +28,7 @@ struct GpuImage {
 
     std::vector<uint32_t> bk_start, bk_ids;
 
-    uint32_t filter_k = 0, filter_bits = 0;
+    uint32_t filter_k = 0, filter_bits = 0, filter_hashes = 1;
     uint64_t filter_paths = 0;
     std::vector<uint32_t> filter;
 
@@ -40,8 +40,9 @@ struct GpuImage {
 };
 
 struct ImageOptions {
-    uint32_t max_filter_bits = 18; // bitmap of 2^bits bits kept in shared memory
-    uint32_t filter_slack = 5;     // bits above log2(#k-grams): density <= 2^-slack
+    uint32_t max_filter_bits = 19; // bitmap of 2^bits bits kept in shared memory (64 KiB)
+    uint32_t filter_slack = 5;     // bits above log2(#k-grams): density <= 2^(1-slack)
+    uint32_t filter_hashes = 2;    // Bloom probes per start
 };
 
 ImageOptions image_options_from_env();

