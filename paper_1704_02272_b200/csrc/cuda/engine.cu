@@ -142,11 +142,10 @@ KernelFn select_kernel(bool grouped, bool identity, int kw)
 {
     using namespace gpu;
     // identity byte maps only exist at sigma = 256, i.e. the grouped layout
-    static const KernelFn table[2][2][3] = {
-        {{pfac_scan_kernel<false, false, 0>, pfac_scan_kernel<false, false, 1>, pfac_scan_kernel<false, false, 2>},
-         {pfac_scan_kernel<false, false, 0>, pfac_scan_kernel<false, false, 1>, pfac_scan_kernel<false, false, 2>}},
-        {{pfac_scan_kernel<true, false, 0>, pfac_scan_kernel<true, false, 1>, pfac_scan_kernel<true, false, 2>},
-         {pfac_scan_kernel<true, true, 0>, pfac_scan_kernel<true, true, 1>, pfac_scan_kernel<true, true, 2>}}};
+#define HFB_KW(G, I) {pfac_scan_kernel<G, I, 0>, pfac_scan_kernel<G, I, 1>, pfac_scan_kernel<G, I, 2>, pfac_scan_kernel<G, I, 3>}
+    static const KernelFn table[2][2][4] = {{HFB_KW(false, false), HFB_KW(false, false)},
+                                            {HFB_KW(true, false), HFB_KW(true, true)}};
+#undef HFB_KW
     return table[grouped][identity && grouped][kw];
 }
 
@@ -158,7 +157,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     d->device = device;
     d->grouped = im.groups != 0;
     d->identity = im.identity && d->grouped;
-    d->kw = im.filter_bits == 0 ? 0 : (im.filter_k <= 4 ? 1 : 2);
+    d->kw = im.filter_bits == 0 ? 0 : (im.filter_k == 4 ? 3 : (im.filter_k < 4 ? 1 : 2));
     d->min_emit = im.min_emit;
     d->reach = im.reach;
     d->node_count = im.node_count;
@@ -192,8 +191,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.min_emit = im.min_emit;
 
     d->kernel = select_kernel(d->grouped, d->identity, d->kw);
-    d->smem = gpu::SmemLayout::text_bytes() + gpu::SmemLayout::queue_bytes() + size_t(v.filter_words) * 4 +
-              (d->identity ? 0 : 512);
+    d->smem = size_t(gpu::kWarps) * gpu::kStages * gpu::kStageBytes + size_t(gpu::kWarps) * gpu::kQueue * 2 + 512 +
+              size_t(v.filter_words) * 4;
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
@@ -223,20 +222,19 @@ struct Workspace {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
     uint8_t* d_text = nullptr;
-    size_t text_cap = 0;
-    hepfac_match_t* d_out = nullptr;   // final, ordered records
-    hepfac_match_t* d_stage = nullptr; // per-tile slices in completion order
+    uint64_t text_cap = 0;
+    hepfac_match_t* d_out = nullptr; // final, ordered records
     uint64_t out_cap = 0;
+    hepfac_match_t* d_stage = nullptr; // per-warp staging regions
+    uint64_t stage_cap = 0, warp_cap = 0;
     uint32_t* d_tile_count = nullptr;
-    unsigned long long* d_tile_slot = nullptr;
-    unsigned long long* d_tile_first = nullptr;
-    uint64_t tile_cap = 0;
+    uint32_t* d_tile_slot = nullptr;
+    uint64_t tile_cap = 0, tile_cap2 = 0;
     unsigned long long* d_chunk = nullptr; // one per CTA of the grid
     uint64_t chunk_cap = 0;
-    // [0] tile counter, [1] total, [2] error word, [3] staging cursor
+    // [0] max records a warp needed (0 = fits), [1] total, [2] error word
     unsigned long long* d_small = nullptr;
-    unsigned long long* h_small = nullptr; // pinned mirror of [1], [2]
-    unsigned long long ctr_base = 0;
+    unsigned long long* h_small = nullptr; // pinned mirror of [0..2]
     uint4* d_flush = nullptr;
     size_t flush_n16 = 0;
 
@@ -253,7 +251,7 @@ struct Workspace {
         cudaSetDevice(device);
         cudaStreamSynchronize(stream);
         for (void* p : {(void*)d_text, (void*)d_out, (void*)d_stage, (void*)d_tile_count, (void*)d_tile_slot,
-                        (void*)d_tile_first, (void*)d_chunk, (void*)d_small, (void*)d_flush})
+                        (void*)d_chunk, (void*)d_small, (void*)d_flush})
             cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
@@ -271,29 +269,18 @@ struct Workspace {
         p = dev_alloc<T>(size_t(n));
         cap = n;
     }
-    void ensure_text(size_t bytes)
+    void ensure_text(uint64_t bytes) { regrow(d_text, text_cap, ((bytes + 15) & ~uint64_t(15)) + 32); }
+    void ensure_out(uint64_t n) { regrow(d_out, out_cap, std::max<uint64_t>(n, 1)); }
+    void ensure_stage(uint64_t warps, uint64_t per_warp)
     {
-        uint64_t cap = text_cap;
-        regrow(d_text, cap, ((bytes + 15) & ~size_t(15)) + 16);
-        text_cap = size_t(cap);
-    }
-    void ensure_out(uint64_t n)
-    {
-        if (n <= out_cap) return;
-        uint64_t c1 = out_cap, c2 = out_cap;
-        regrow(d_out, c1, n);
-        regrow(d_stage, c2, n);
-        out_cap = n;
+        warp_cap = std::max(warp_cap, per_warp);
+        regrow(d_stage, stage_cap, warps * warp_cap);
+        warp_cap = stage_cap / warps; // a bigger region from an earlier grid is reused
     }
     void ensure_tiles(uint64_t tiles, uint64_t grid)
     {
-        if (tiles > tile_cap) {
-            uint64_t a = tile_cap, b = tile_cap, c = tile_cap;
-            regrow(d_tile_count, a, tiles);
-            regrow(d_tile_slot, b, tiles);
-            regrow(d_tile_first, c, tiles);
-            tile_cap = tiles;
-        }
+        regrow(d_tile_count, tile_cap, tiles);
+        regrow(d_tile_slot, tile_cap2, tiles);
         regrow(d_chunk, chunk_cap, grid);
     }
 };
@@ -331,19 +318,34 @@ struct WorkspaceLease {
 
 thread_local ScanStats t_stats;
 
-// Enqueue one cooperative launch over device-resident text.  The tile
-// counter is never reset: each launch consumes exactly n_tiles + 3 * grid
-// increments (see pfac_scan_kernel).
+// Expected records per text byte before the first run tells us better.
+uint64_t initial_records(uint64_t bytes) { return std::max<uint64_t>(1u << 14, bytes / 256); }
+
+struct Launch {
+    uint64_t n_tiles = 0, grid = 0, warps = 0;
+};
+
+Launch plan(const DeviceTrie& dt, uint64_t n_own)
+{
+    Launch l;
+    l.n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
+    l.grid = std::min<uint64_t>(uint64_t(dt.sm_count) * dt.blocks_per_sm,
+                                std::max<uint64_t>(1, (l.n_tiles + gpu::kWarps - 1) / gpu::kWarps));
+    l.warps = l.grid * gpu::kWarps;
+    return l;
+}
+
+// Enqueue one cooperative launch over device-resident text (no host sync).
 uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text, uint64_t n_own,
                       uint64_t n_avail, uint64_t g0)
 {
-    const uint64_t n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
-    if (n_tiles == 0) {
-        CK(cudaMemsetAsync(ws.d_small + 1, 0, sizeof(unsigned long long), ws.stream));
-        return 0;
-    }
-    const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(dt.sm_count) * dt.blocks_per_sm);
-    ws.ensure_tiles(n_tiles, grid);
+    CK(cudaMemsetAsync(ws.d_small, 0, 3 * sizeof(unsigned long long), ws.stream));
+    const Launch l = plan(dt, n_own);
+    if (l.n_tiles == 0) return 0;
+    ws.ensure_tiles(l.n_tiles, l.grid);
+    if (ws.warp_cap == 0) ws.ensure_stage(l.warps, initial_records(n_own) / l.warps + 64);
+    ws.ensure_stage(l.warps, ws.warp_cap);
+    if (ws.out_cap == 0) ws.ensure_out(initial_records(n_own));
     gpu::ScanArgs a{};
     a.trie = dt.view;
     a.text = d_text;
@@ -351,48 +353,68 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
     a.n_avail = n_avail;
     a.g0 = g0;
     a.out = ws.d_out;
+    a.out_cap = ws.out_cap;
     a.stage = ws.d_stage;
-    a.cap = ws.out_cap;
-    a.tile_ctr = ws.d_small;
-    a.tile_base = ws.ctr_base;
-    a.n_tiles = n_tiles;
+    a.warp_cap = ws.warp_cap;
+    a.n_tiles = l.n_tiles;
     a.tile_count = ws.d_tile_count;
     a.tile_slot = ws.d_tile_slot;
-    a.tile_first = ws.d_tile_first;
     a.chunk_sum = ws.d_chunk;
-    a.stage_cursor = ws.d_small + 3;
     a.total = ws.d_small + 1;
+    a.warp_need = ws.d_small;
     a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
     void* params[] = {&a};
-    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(grid)),
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(l.grid)),
                                                       dim3(gpu::kThreads), params, dt.smem, ws.stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        // the counter state is unknown after a failed launch: reset it
-        cudaMemset(ws.d_small, 0, 4 * sizeof(unsigned long long));
-        ws.ctr_base = 0;
         cuda_fail(e, "pfac_scan_kernel launch");
     }
-    ws.ctr_base += n_tiles + 3 * grid;
     return 1;
 }
 
-void fetch_small(Workspace& ws)
+// Reads back [warp_need, total, err]; true when the results are complete.
+bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own)
 {
-    CK(cudaMemcpyAsync(ws.h_small, ws.d_small + 1, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       ws.stream));
+    CK(cudaMemcpyAsync(ws.h_small, ws.d_small, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
-    if (ws.h_small[1] & 1u)
-        fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
+    if (ws.h_small[2] & 1u) fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
+    bool ok = true;
+    if (ws.h_small[0]) { // some warp's staging region overflowed
+        const Launch l = plan(dt, n_own);
+        ws.ensure_stage(l.warps, ws.h_small[0] + ws.h_small[0] / 4 + 64);
+        ok = false;
+    }
+    if (ws.h_small[1] > ws.out_cap) {
+        ws.ensure_out(ws.h_small[1]);
+        ok = false;
+    }
+    return ok;
 }
-
-uint64_t initial_capacity(uint64_t bytes) { return std::max<uint64_t>(1u << 16, bytes / 64); }
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b)
 {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, a, b));
     return double(ms);
+}
+
+// Scan of device-resident text, re-run with grown buffers until complete.
+uint64_t run_to_completion(const DeviceTrie& dt, Workspace& ws, uint64_t n_own, uint64_t n_avail, uint64_t g0,
+                           ScanStats* st)
+{
+    for (int attempt = 0;; ++attempt) {
+        if (st) CK(cudaEventRecord(ws.ev[1], ws.stream));
+        const uint32_t k = enqueue_scan(dt, ws, ws.d_text, n_own, n_avail, g0);
+        if (st) {
+            CK(cudaEventRecord(ws.ev[2], ws.stream));
+            st->kernel_launches += k;
+        }
+        if (!k) return 0;
+        if (fetch_small(ws, dt, n_own)) return ws.h_small[1];
+        if (st) st->relaunches++;
+        if (attempt > 4) fail(HEPFAC_ERR_INTERNAL, "scan buffers keep overflowing");
+    }
 }
 
 // Copies `text` in, scans, copies the sorted list out.  The whole text goes to
@@ -418,24 +440,9 @@ std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uin
     }
     WorkspaceLease ws(dev);
     ws->ensure_text(avail);
-    ws->ensure_out(std::max(ws->out_cap, initial_capacity(owned)));
-    CK(cudaMemsetAsync(ws->d_small + 2, 0, sizeof(unsigned long long), ws->stream));
     CK(cudaEventRecord(ws->ev[0], ws->stream));
     CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
-    CK(cudaEventRecord(ws->ev[1], ws->stream));
-    st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0);
-    CK(cudaEventRecord(ws->ev[2], ws->stream));
-    fetch_small(*ws);
-    uint64_t total = ws->h_small[0];
-    if (total > ws->out_cap) { // overflow: re-run with the exact size
-        ws->ensure_out(total);
-        CK(cudaEventRecord(ws->ev[1], ws->stream));
-        st.kernel_launches += enqueue_scan(*dt, *ws, ws->d_text, owned, avail, g0);
-        CK(cudaEventRecord(ws->ev[2], ws->stream));
-        fetch_small(*ws);
-        total = ws->h_small[0];
-        st.relaunches = 1;
-    }
+    const uint64_t total = run_to_completion(*dt, *ws, owned, avail, g0, &st);
     out->allocate(size_t(total));
     if (total)
         CK(cudaMemcpyAsync(out->data, ws->d_out, size_t(total) * sizeof(hepfac_match_t), cudaMemcpyDeviceToHost,
@@ -513,19 +520,15 @@ Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes
     ws->ensure_text(bytes);
     CK(cudaMemcpy(ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
     if (dt->min_emit == UINT32_MAX || bytes < dt->min_emit) return r;
-    ws->ensure_out(std::max(ws->out_cap, initial_capacity(bytes)));
-    CK(cudaMemsetAsync(ws->d_small + 2, 0, sizeof(unsigned long long), ws->stream));
-    enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0); // warm-up, untimed
-    fetch_small(*ws);
-    ws->ensure_out(ws->h_small[0]);
+    run_to_completion(*dt, *ws, bytes, bytes, 0, nullptr); // warm-up, untimed; sizes the buffers
     std::vector<hepfac_match_t> host;
     double sum_scan = 0, sum_merge = 0;
     for (uint32_t i = 0; i < runs; ++i) {
         CK(cudaEventRecord(ws->ev[0], ws->stream));
         enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0);
         CK(cudaEventRecord(ws->ev[1], ws->stream));
-        fetch_small(*ws);
-        r.matches = ws->h_small[0];
+        if (!fetch_small(*ws, *dt, bytes)) fail(HEPFAC_ERR_INTERNAL, "scan buffers overflowed after warm-up");
+        r.matches = ws->h_small[1];
         host.resize(size_t(r.matches));
         CK(cudaEventRecord(ws->ev[2], ws->stream));
         if (r.matches)
@@ -548,6 +551,7 @@ struct Session {
     std::shared_ptr<DeviceTrie> dt;
     std::unique_ptr<Workspace> ws;
     uint64_t bytes = 0, matches = 0, offset = 0, owned = 0;
+    bool complete = false;
     std::vector<cudaEvent_t> evs;
     ~Session()
     {
@@ -571,7 +575,6 @@ Session* session_create(const Trie& t, const uint8_t* text, uint64_t bytes, uint
     s->owned = owned;
     s->ws->ensure_text(bytes);
     CK(cudaMemcpy(s->ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
-    s->ws->ensure_out(initial_capacity(bytes));
     return s.release();
 }
 
@@ -592,7 +595,6 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventCreate(&e));
         s->evs.push_back(e);
     }
-    CK(cudaMemsetAsync(ws.d_small + 2, 0, sizeof(unsigned long long), ws.stream));
     for (uint32_t i = 0; i < iterations; ++i) {
         if (flush_l2)
             gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
@@ -600,11 +602,10 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset);
         CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
     }
-    fetch_small(ws);
-    s->matches = can_match ? ws.h_small[0] : 0;
+    s->complete = !can_match || fetch_small(ws, dt, s->owned); // grows buffers for the next run
+    s->matches = can_match ? ws.h_small[1] : 0;
     for (uint32_t i = 0; i < iterations; ++i)
         if (ms_each) ms_each[i] = elapsed_ms(s->evs[2 * i], s->evs[2 * i + 1]);
-    if (s->matches > ws.out_cap) ws.ensure_out(s->matches); // next run stores everything
 }
 
 uint64_t session_matches(Session* s) { return s->matches; }
@@ -613,7 +614,7 @@ std::unique_ptr<MatchList> session_fetch(Session* s)
 {
     Workspace& ws = *s->ws;
     DeviceGuard g(ws.device);
-    if (s->matches > ws.out_cap) fail(HEPFAC_ERR_STATE, "session results overflowed: run again before fetching");
+    if (!s->complete) fail(HEPFAC_ERR_STATE, "session results overflowed: run again before fetching");
     auto out = std::make_unique<MatchList>();
     out->allocate(size_t(s->matches));
     if (s->matches)

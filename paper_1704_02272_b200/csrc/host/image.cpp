@@ -285,10 +285,10 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             im.filter.assign((size_t(1) << bits) / 32, 0u);
             for (uint64_t g : grams) {
                 const uint32_t s = k <= 4 ? filter_slot32(uint32_t(g), bits) : filter_slot64(g, bits);
-                im.filter[s >> 5] |= 1u << (s & 31);
+                im.filter[s >> 5] |= 0x80000000u >> (s & 31); // MSB-first (probe_into)
                 if (im.filter_hashes > 1) {
                     const uint32_t s2 = k <= 4 ? filter_slot32b(uint32_t(g), bits) : filter_slot64b(g, bits);
-                    im.filter[s2 >> 5] |= 1u << (s2 & 31);
+                    im.filter[s2 >> 5] |= 0x80000000u >> (s2 & 31);
                 }
             }
         }
