@@ -45,7 +45,7 @@ constexpr uint32_t kLaneStarts = 16;                 // consecutive starts per l
 constexpr uint32_t kGroup = 32 * kLaneStarts;         // 512 starts per warp group
 constexpr uint32_t kGroupsPerTile = 16;
 constexpr uint32_t kTile = kGroup * kGroupsPerTile;   // 8192 starts per warp-tile
-constexpr uint32_t kQueue = 256;                      // per-warp survivor queue (entries)
+constexpr uint32_t kQueue = kGroup;                   // per-warp survivor queue (>= one group)
 constexpr uint32_t kStages = 3;                       // per-warp TMA ring depth (groups in flight)
 constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the 8-byte key overhang, 16-aligned
 constexpr uint32_t kRegRecords = 2;                   // records a lane keeps per walk round

@@ -40,9 +40,9 @@ struct GpuImage {
 };
 
 struct ImageOptions {
-    uint32_t max_filter_bits = 19; // bitmap of 2^bits bits kept in shared memory (64 KiB)
-    uint32_t filter_slack = 5;     // bits above log2(#k-grams): density <= 2^(1-slack)
-    uint32_t filter_hashes = 2;    // Bloom probes per start
+    uint32_t max_filter_bits = 20; // bitmap of 2^bits bits kept in shared memory (128 KiB)
+    uint32_t filter_slack = 6;     // bits above log2(#k-grams): density <= 2^-slack
+    uint32_t filter_hashes = 1;    // Bloom probes per start
 };
 
 ImageOptions image_options_from_env();
