@@ -39,14 +39,20 @@ namespace hfb::gpu {
 
 namespace cg = cooperative_groups;
 
-constexpr uint32_t kThreads = 1024;
-constexpr uint32_t kWarps = kThreads / 32;
+#ifndef HFB_WARPS
+#define HFB_WARPS 32
+#endif
+#ifndef HFB_STAGES
+#define HFB_STAGES 3
+#endif
+constexpr uint32_t kWarps = HFB_WARPS; // warps per CTA (one CTA per SM)
+constexpr uint32_t kThreads = kWarps * 32;
 constexpr uint32_t kLaneStarts = 16;                 // consecutive starts per lane per group
 constexpr uint32_t kGroup = 32 * kLaneStarts;         // 512 starts per warp group
 constexpr uint32_t kGroupsPerTile = 16;
 constexpr uint32_t kTile = kGroup * kGroupsPerTile;   // 8192 starts per warp-tile
 constexpr uint32_t kQueue = kGroup;                   // per-warp survivor queue (>= one group)
-constexpr uint32_t kStages = 3;                       // per-warp TMA ring depth (groups in flight)
+constexpr uint32_t kStages = HFB_STAGES;              // per-warp TMA ring depth (groups in flight)
 constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the 8-byte key overhang, 16-aligned
 constexpr uint32_t kRegRecords = 2;                   // records a lane keeps per walk round
 
@@ -262,10 +268,10 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
     if (lane == 0) s_scr[warp] = wt;
     __syncthreads();
     if (warp == 0) {
-        const uint32_t x = s_scr[lane];
+        const uint32_t x = lane < kWarps ? s_scr[lane] : 0u;
         uint32_t tt;
         const uint32_t xe = warp_exclusive(x, lane, tt);
-        s_scr[lane] = xe;
+        if (lane < kWarps) s_scr[lane] = xe;
         if (lane == 0) s_scr[kWarps] = tt;
     }
     __syncthreads();
@@ -317,6 +323,7 @@ struct Walker {
             }
             produced += tot;
         }
+        cursor += produced; // later drains of the same tile append after these
         return produced;
     }
 };
@@ -380,59 +387,63 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint8_t* ring = s_ring + warp * kStages * kStageBytes;
     uint64_t* bars = s_bar[warp];
 
-    // The warp's groups form one sequence q = 0, 1, ...: tile gw + (q / 16) W,
-    // group q % 16.  Lane 0 keeps kStages of them in flight.
-    const uint64_t my_tiles = gw < a.n_tiles ? (a.n_tiles - gw + W - 1) / W : 0;
-    const uint64_t n_groups = my_tiles * kGroupsPerTile;
-    auto group_addr = [&](uint64_t q) {
-        return (gw + (q / kGroupsPerTile) * uint64_t(W)) * kTile + (q % kGroupsPerTile) * kGroup;
-    };
-    auto issue = [&](uint64_t q) { // lane 0 only
-        if (q >= n_groups) return;
-        const uint64_t p = group_addr(q);
-        if (p >= avail16) return; // nothing to fetch: consumers skip the wait too
-        const uint32_t n = uint32_t(min(uint64_t(kStageBytes), avail16 - p));
-        bulk_load(ring + (q % kStages) * kStageBytes, a.text + p, n, &bars[q % kStages]);
+    // Producer (lane 0): walks the warp's group sequence -- tile gw, gw + W,
+    // ...; 16 groups each -- and keeps kStages groups in flight.  Groups past
+    // the text end are skipped by producer and consumer alike, so both sides
+    // see the same stage order.
+    uint64_t p_tile = gw;
+    uint32_t p_g = 0, p_stage = 0;
+    auto produce = [&]() {
+        for (;;) {
+            if (p_tile >= a.n_tiles) return;
+            const uint64_t p = p_tile * kTile + p_g * kGroup;
+            if (++p_g == kGroupsPerTile) p_g = 0, p_tile += W;
+            if (p >= avail16) continue;
+            const uint32_t n = uint32_t(min(uint64_t(kStageBytes), avail16 - p));
+            bulk_load(ring + p_stage * kStageBytes, a.text + p, n, &bars[p_stage]);
+            p_stage = p_stage + 1 == kStages ? 0u : p_stage + 1;
+            return;
+        }
     };
     if (lane == 0) {
         for (uint32_t s = 0; s < kStages; ++s) mbar_init(&bars[s]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (uint32_t s = 0; s < kStages; ++s) issue(s);
+        for (uint32_t s = 0; s < kStages; ++s) produce();
     }
     __syncthreads(); // filter, symbol map and barrier inits visible
 
     Walker<GROUPED, IDENT> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
-    uint64_t q = 0;
+    uint32_t c_stage = 0, c_parity = 0;
+    const uint8_t* my_bytes = ring + lane * kLaneStarts;
     for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
         const uint64_t lo = tile * kTile;
         const uint64_t slot = wk.cursor;
-        uint32_t qn = 0, recs = 0;
-        for (uint32_t g = 0; g < kGroupsPerTile; ++g, ++q) {
-            const uint64_t o0 = lo + g * kGroup + lane * kLaneStarts;
-            uint32_t valid = 0;
-            if (o0 < start_end) {
-                const uint64_t r = start_end - o0;
-                valid = r >= kLaneStarts ? 0xFFFFu : ((1u << r) - 1u);
-            }
+        // tile-relative limits (32-bit): starts that may report, groups fetched
+        const uint32_t rem = start_end > lo ? uint32_t(min(start_end - lo, uint64_t(kTile))) : 0u;
+        const uint32_t fetched = lo < avail16 ? uint32_t(min((avail16 - lo + kGroup - 1) / kGroup,
+                                                             uint64_t(kGroupsPerTile)))
+                                              : 0u;
+        uint32_t qn = 0;
+        for (uint32_t g = 0; g < fetched; ++g) {
+            const int32_t r = int32_t(rem) - int32_t(g * kGroup + lane * kLaneStarts);
+            const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            mbar_wait(&bars[c_stage], c_parity);
             uint32_t mask = 0;
-            if (lo + g * kGroup < avail16) { // the stage was fetched: consume it
-                const uint32_t stage = uint32_t(q % kStages);
-                mbar_wait(&bars[stage], uint32_t(q / kStages) & 1u);
-                const uint8_t* src = ring + stage * kStageBytes + lane * kLaneStarts;
-                if (__any_sync(0xFFFFFFFFu, valid)) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(src);
-                    const uint2 x = *reinterpret_cast<const uint2*>(src + 16);
-                    const uint32_t w[6] = {v.x, v.y, v.z, v.w, x.x, x.y};
-                    mask = filter_mask<KW>(t, w, s_filter, valid);
-                }
-                __syncwarp();
-                if (lane == 0) issue(q + kStages); // refill the stage just consumed
+            if (__any_sync(0xFFFFFFFFu, valid)) {
+                const uint8_t* src = my_bytes + c_stage * kStageBytes;
+                const uint4 v = *reinterpret_cast<const uint4*>(src);
+                const uint2 x = *reinterpret_cast<const uint2*>(src + 16);
+                const uint32_t w[6] = {v.x, v.y, v.z, v.w, x.x, x.y};
+                mask = filter_mask<KW>(t, w, s_filter, valid);
             }
+            __syncwarp();
+            if (lane == 0) produce(); // refill the stage just consumed
+            if (++c_stage == kStages) c_stage = 0, c_parity ^= 1u;
 
             uint32_t tot;
             const uint32_t ex = warp_exclusive(__popc(mask), lane, tot);
             if (qn + tot > kQueue) { // warp-uniform: flush the queue first
-                recs += wk.drain(lo, qn);
+                wk.drain(lo, qn);
                 qn = 0;
                 __syncwarp();
             }
@@ -442,11 +453,10 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
             qn += tot;
             __syncwarp();
         }
-        recs += wk.drain(lo, qn);
+        wk.drain(lo, qn);
         __syncwarp();
-        wk.cursor += recs;
         if (lane == 0) {
-            a.tile_count[tile] = recs;
+            a.tile_count[tile] = uint32_t(wk.cursor - slot);
             a.tile_slot[tile] = uint32_t(slot);
         }
     }

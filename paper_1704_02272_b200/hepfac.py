@@ -21,7 +21,7 @@ from typing import Iterable, Optional, Sequence, Union
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libhepfac.so")
+LIB_PATH = os.environ.get("HEPFAC_LIB") or os.path.join(PKG_DIR, "libhepfac.so")
 
 MATCH_DTYPE = np.dtype([("start", "<u8"), ("length", "<u4"), ("pattern_id", "<u4")])
 NO_NODE = 0xFFFFFFFF
