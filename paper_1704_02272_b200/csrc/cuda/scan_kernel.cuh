@@ -71,6 +71,8 @@ struct ScanArgs {
     uint32_t* tile_slot;    // offset of the tile's records inside its warp's region
     unsigned long long* chunk_sum;
     unsigned long long* total;
+    const unsigned long long* base_in; // records placed by earlier launches of a streamed scan
+    unsigned long long* base_out;      // base_in + this launch's total (distinct word)
     unsigned long long* warp_need; // max records any warp needed (overflow sizing)
     unsigned int* err;
 };
@@ -93,9 +95,11 @@ __device__ __noinline__ bool same_bytes(const ScanArgs& a, uint64_t start, uint3
 // Shared terminal: identify the slice by its key, then confirm byte-wise
 // (the reference's dictionary lookup, trie.hpp:103-107; a miss is its
 // logic_error "terminal node spells no dictionary pattern", scan.cpp:34).
-__device__ __noinline__ uint32_t resolve_slice(const ScanArgs& a, uint64_t start, uint32_t len, uint64_t h)
+__device__ __noinline__ uint32_t resolve_slice(const ScanArgs& a, uint64_t start, uint32_t len)
 {
     const TrieView& t = a.trie;
+    uint64_t h = 0; // the slice key is computed only here, off the per-step path
+    for (uint32_t i = 0; i < len; ++i) h = slice_step(h, t.hmul, text_byte(a, start + i));
     const uint64_t key = slice_key(h, len);
     for (uint64_t s = mix64(key) & t.ht_mask;; s = (s + 1) & t.ht_mask) {
         const uint32_t id = __ldg(t.ht_id + s);
@@ -153,17 +157,20 @@ template <bool GROUPED, bool IDENT>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, Sink& sink)
 {
     const TrieView& t = a.trie;
+    const uint8_t* txt = a.text + start;
+    // bytes this walk may consume before the text (or shard halo) ends
+    const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
+    const uint32_t limit = t.depth_limit ? t.depth_limit : 0xFFFFFFFFu;
     uint32_t node = 0, depth = 0;
-    uint64_t pos = start, h = 0;
     for (;;) {
-        const bool more = pos < a.n_avail;
-        const uint32_t byte = more ? text_byte(a, pos) : 0u;
+        const bool more = depth < room;
+        const uint32_t byte = more ? uint32_t(__ldg(txt + depth)) : 0u;
         const uint32_t sym = IDENT ? byte : uint32_t(s_sym[byte]);
         const bool step = more && (IDENT || sym != kNoSym);
         uint32_t word, base, meta, inline_id = kNoId;
         if (GROUPED) {
             const uint32_t g = step ? (sym >> 6) : 0u;
-            const uint4 r = __ldg(reinterpret_cast<const uint4*>(t.nodes) + size_t(node) * t.groups + g);
+            const uint4 r = __ldg(reinterpret_cast<const uint4*>(t.nodes) + (node * t.groups + g));
             const bool hi = (sym >> 5) & 1u;
             word = hi ? r.y : r.x;
             base = (r.z & kBaseMask) + (hi ? uint32_t(__popc(r.x)) : 0u);
@@ -175,25 +182,23 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
             base = r.y & kBaseMask;
             meta = r.y;
         }
-        if (depth) {
-            if (meta & kFlagTerminal) {
+        if (meta & (kFlagTerminal | kFlagBucket)) {
+            if (depth && (meta & kFlagTerminal)) {
                 uint32_t id = GROUPED ? inline_id : __ldg(t.term_id + node);
-                if (id == kNoId) id = resolve_slice(a, start, depth, h);
+                if (id == kNoId) id = resolve_slice(a, start, depth);
                 if (id == kNoId) atomicOr(a.err, 1u);
                 else sink.put(a.g0 + start, depth, id);
             }
-            if (depth == t.depth_limit) {
-                if (meta & kFlagBucket) verify_bucket(a, node, start, sink);
-                break;
-            }
+        }
+        if (depth == limit) { // depth-limit nodes are leaves (scan.cpp:37-49)
+            if (meta & kFlagBucket) verify_bucket(a, node, start, sink);
+            break;
         }
         if (!step) break;
         const uint32_t b = sym & 31u;
         if (!((word >> b) & 1u)) break;
         node = base + uint32_t(__popc(word & ((1u << b) - 1u)));
-        ++pos;
         ++depth;
-        h = slice_step(h, t.hmul, byte);
     }
 }
 
@@ -477,14 +482,18 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     grid.sync();
 
     // phase 3: scan the chunk, copy staged slices to their final offsets
-    unsigned long long base = 0, total = 0;
+    const unsigned long long origin = *a.base_in;
+    unsigned long long base = origin, total = 0;
     for (uint32_t b = 0; b < gridDim.x; ++b) {
         const unsigned long long v = a.chunk_sum[b];
         base += b < blockIdx.x ? v : 0ull;
         total += v;
     }
-    if (blockIdx.x == gridDim.x - 1 && tid == 0) *a.total = total;
-    const bool fits = total <= a.out_cap && *a.warp_need == 0;
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+        *a.total = total;
+        *a.base_out = origin + total;
+    }
+    const bool fits = origin + total <= a.out_cap && *a.warp_need == 0;
     for (uint64_t r0 = c0; r0 < c1; r0 += kThreads) {
         const uint64_t i = r0 + tid;
         const uint32_t n = i < c1 ? a.tile_count[i] : 0u;
