@@ -219,10 +219,14 @@ namespace {
 
 struct Workspace {
     int device = 0;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {};
+    cudaStream_t stream = nullptr; // kernels (and D2H)
+    cudaStream_t copy = nullptr;   // H2D of streamed chunks
+    cudaEvent_t ev[6] = {};
+    cudaEvent_t h2d_done[2] = {}, kern_done[2] = {};
     uint8_t* d_text = nullptr;
     uint64_t text_cap = 0;
+    uint8_t* d_slot[2] = {};       // streamed chunk buffers
+    uint64_t slot_cap = 0;
     hepfac_match_t* d_out = nullptr; // final, ordered records
     uint64_t out_cap = 0;
     hepfac_match_t* d_stage = nullptr; // per-warp staging regions
@@ -232,29 +236,41 @@ struct Workspace {
     uint64_t tile_cap = 0, tile_cap2 = 0;
     unsigned long long* d_chunk = nullptr; // one per CTA of the grid
     uint64_t chunk_cap = 0;
-    // [0] max records a warp needed (0 = fits), [1] total, [2] error word
+    unsigned long long* d_bases = nullptr; // streamed: records before chunk c
+    uint64_t bases_cap = 0;
+    // [0] max records a warp needed (0 = fits), [1] total of the last launch,
+    // [2] error word, [3] zero (base_in of a single launch), [4] its base_out
     unsigned long long* d_small = nullptr;
-    unsigned long long* h_small = nullptr; // pinned mirror of [0..2]
+    unsigned long long* h_small = nullptr; // pinned mirror
     uint4* d_flush = nullptr;
     size_t flush_n16 = 0;
 
     explicit Workspace(int dev) : device(dev)
     {
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
         for (auto& e : ev) CK(cudaEventCreate(&e));
-        d_small = dev_alloc<unsigned long long>(4);
-        CK(cudaMemset(d_small, 0, 4 * sizeof(unsigned long long)));
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_small), 4 * sizeof(unsigned long long), cudaHostAllocDefault));
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaEventCreateWithFlags(&h2d_done[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&kern_done[k], cudaEventDisableTiming));
+        }
+        d_small = dev_alloc<unsigned long long>(8);
+        CK(cudaMemset(d_small, 0, 8 * sizeof(unsigned long long)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_small), 8 * sizeof(unsigned long long), cudaHostAllocDefault));
     }
     ~Workspace()
     {
         cudaSetDevice(device);
         cudaStreamSynchronize(stream);
-        for (void* p : {(void*)d_text, (void*)d_out, (void*)d_stage, (void*)d_tile_count, (void*)d_tile_slot,
-                        (void*)d_chunk, (void*)d_small, (void*)d_flush})
+        cudaStreamSynchronize(copy);
+        for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
+                        (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
+                        (void*)d_flush})
             cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
+        for (int k = 0; k < 2; ++k) cudaEventDestroy(h2d_done[k]), cudaEventDestroy(kern_done[k]);
+        cudaStreamDestroy(copy);
         cudaStreamDestroy(stream);
     }
 
@@ -263,13 +279,23 @@ struct Workspace {
     {
         if (n <= cap) return;
         CK(cudaStreamSynchronize(stream));
+        CK(cudaStreamSynchronize(copy));
         cudaFree(p);
         p = nullptr;
         cap = 0;
         p = dev_alloc<T>(size_t(n));
         cap = n;
     }
-    void ensure_text(uint64_t bytes) { regrow(d_text, text_cap, ((bytes + 15) & ~uint64_t(15)) + 32); }
+    static uint64_t padded(uint64_t bytes) { return ((bytes + 15) & ~uint64_t(15)) + 32; }
+    void ensure_text(uint64_t bytes) { regrow(d_text, text_cap, padded(bytes)); }
+    void ensure_slots(uint64_t bytes)
+    {
+        if (padded(bytes) <= slot_cap) return;
+        uint64_t c0 = slot_cap, c1 = slot_cap;
+        regrow(d_slot[0], c0, padded(bytes));
+        regrow(d_slot[1], c1, padded(bytes));
+        slot_cap = c0;
+    }
     void ensure_out(uint64_t n) { regrow(d_out, out_cap, std::max<uint64_t>(n, 1)); }
     void ensure_stage(uint64_t warps, uint64_t per_warp)
     {
@@ -283,6 +309,8 @@ struct Workspace {
         regrow(d_tile_slot, tile_cap2, tiles);
         regrow(d_chunk, chunk_cap, grid);
     }
+    // Clears the per-scan accumulators (overflow need, error word).
+    void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 5 * sizeof(unsigned long long), stream)); }
 };
 
 std::mutex g_pool_mu;
@@ -336,12 +364,18 @@ Launch plan(const DeviceTrie& dt, uint64_t n_own)
 }
 
 // Enqueue one cooperative launch over device-resident text (no host sync).
+// Its records land at [*base_in, *base_in + total) of the output; the launch
+// stores *base_in + total to *base_out.
 uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text, uint64_t n_own,
-                      uint64_t n_avail, uint64_t g0)
+                      uint64_t n_avail, uint64_t g0, const unsigned long long* base_in = nullptr,
+                      unsigned long long* base_out = nullptr)
 {
-    CK(cudaMemsetAsync(ws.d_small, 0, 3 * sizeof(unsigned long long), ws.stream));
     const Launch l = plan(dt, n_own);
-    if (l.n_tiles == 0) return 0;
+    if (!base_in) base_in = ws.d_small + 3, base_out = ws.d_small + 4;
+    if (l.n_tiles == 0) {
+        CK(cudaMemcpyAsync(base_out, base_in, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ws.stream));
+        return 0;
+    }
     ws.ensure_tiles(l.n_tiles, l.grid);
     if (ws.warp_cap == 0) ws.ensure_stage(l.warps, initial_records(n_own) / l.warps + 64);
     ws.ensure_stage(l.warps, ws.warp_cap);
@@ -361,6 +395,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
     a.tile_slot = ws.d_tile_slot;
     a.chunk_sum = ws.d_chunk;
     a.total = ws.d_small + 1;
+    a.base_in = base_in;
+    a.base_out = base_out;
     a.warp_need = ws.d_small;
     a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
     void* params[] = {&a};
@@ -373,10 +409,13 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
     return 1;
 }
 
-// Reads back [warp_need, total, err]; true when the results are complete.
-bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own)
+// Reads back the scan's accumulators; true when the results are complete.
+// `records` is the word holding the scan's final record count.
+bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own, const unsigned long long* records = nullptr)
 {
+    if (!records) records = ws.d_small + 4;
     CK(cudaMemcpyAsync(ws.h_small, ws.d_small, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(ws.h_small + 4, records, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
     if (ws.h_small[2] & 1u) fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
     bool ok = true;
@@ -385,12 +424,14 @@ bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own)
         ws.ensure_stage(l.warps, ws.h_small[0] + ws.h_small[0] / 4 + 64);
         ok = false;
     }
-    if (ws.h_small[1] > ws.out_cap) {
-        ws.ensure_out(ws.h_small[1]);
+    if (ws.h_small[4] > ws.out_cap) {
+        ws.ensure_out(ws.h_small[4]);
         ok = false;
     }
     return ok;
 }
+
+uint64_t records_of(const Workspace& ws) { return ws.h_small[4]; }
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b)
 {
@@ -404,6 +445,7 @@ uint64_t run_to_completion(const DeviceTrie& dt, Workspace& ws, uint64_t n_own, 
                            ScanStats* st)
 {
     for (int attempt = 0;; ++attempt) {
+        ws.begin_scan();
         if (st) CK(cudaEventRecord(ws.ev[1], ws.stream));
         const uint32_t k = enqueue_scan(dt, ws, ws.d_text, n_own, n_avail, g0);
         if (st) {
@@ -411,15 +453,63 @@ uint64_t run_to_completion(const DeviceTrie& dt, Workspace& ws, uint64_t n_own, 
             st->kernel_launches += k;
         }
         if (!k) return 0;
-        if (fetch_small(ws, dt, n_own)) return ws.h_small[1];
+        if (fetch_small(ws, dt, n_own)) return records_of(ws);
         if (st) st->relaunches++;
         if (attempt > 4) fail(HEPFAC_ERR_INTERNAL, "scan buffers keep overflowing");
     }
 }
 
-// Copies `text` in, scans, copies the sorted list out.  The whole text goes to
-// the device in one piece (HBM holds 180 GB); the H2D copy, kernel and D2H
-// run back to back on one stream.
+uint64_t stream_chunk_bytes()
+{
+    uint64_t c = uint64_t(64) << 20;
+    if (const char* s = std::getenv("HEPFAC_CHUNK_MIB")) {
+        const long v = std::strtol(s, nullptr, 10);
+        if (v >= 1 && v <= (1 << 20)) c = uint64_t(v) << 20;
+    }
+    return c;
+}
+
+// Streamed scan of host text: chunks of starts go H2D on the copy stream into
+// two device slots while the previous chunk's launch runs on the compute
+// stream; each launch places its records right after the previous chunk's
+// (device-side running base), so the output is ordered without host syncs
+// between chunks.  Chunk c's bytes carry the `halo` of right context its last
+// starts may read.
+uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, uint64_t avail, uint64_t owned,
+                     uint64_t g0, uint64_t halo, ScanStats& st)
+{
+    const uint64_t C = stream_chunk_bytes();
+    const uint64_t n = (owned + C - 1) / C;
+    ws.ensure_slots(std::min(avail, C + halo));
+    ws.regrow(ws.d_bases, ws.bases_cap, n + 1);
+    for (int attempt = 0;; ++attempt) {
+        ws.begin_scan();
+        CK(cudaMemsetAsync(ws.d_bases, 0, sizeof(unsigned long long), ws.stream));
+        CK(cudaEventRecord(ws.ev[0], ws.stream));
+        CK(cudaStreamWaitEvent(ws.copy, ws.ev[0], 0));
+        for (uint64_t c = 0; c < n; ++c) {
+            const int slot = int(c & 1);
+            const uint64_t lo = c * C, own = std::min(C, owned - lo), bytes = std::min(avail - lo, own + halo);
+            if (c >= 2) CK(cudaStreamWaitEvent(ws.copy, ws.kern_done[slot], 0));
+            CK(cudaMemcpyAsync(ws.d_slot[slot], text + lo, size_t(bytes), cudaMemcpyHostToDevice, ws.copy));
+            CK(cudaEventRecord(ws.h2d_done[slot], ws.copy));
+            CK(cudaStreamWaitEvent(ws.stream, ws.h2d_done[slot], 0));
+            if (c == 0) CK(cudaEventRecord(ws.ev[1], ws.stream));
+            st.kernel_launches +=
+                enqueue_scan(dt, ws, ws.d_slot[slot], own, bytes, g0 + lo, ws.d_bases + c, ws.d_bases + c + 1);
+            CK(cudaEventRecord(ws.kern_done[slot], ws.stream));
+        }
+        CK(cudaEventRecord(ws.ev[2], ws.stream));
+        st.chunks = uint32_t(n);
+        if (fetch_small(ws, dt, C, ws.d_bases + n)) return records_of(ws);
+        st.relaunches++;
+        if (attempt > 4) fail(HEPFAC_ERR_INTERNAL, "scan buffers keep overflowing");
+    }
+}
+
+// Copies `text` in, scans, copies the sorted list out.  Texts up to two chunks
+// go to the device in one piece; longer ones are streamed chunk by chunk so
+// the H2D copy overlaps the kernels.
 std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,
                                          uint64_t g0)
 {
@@ -439,22 +529,28 @@ std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uin
         return out;
     }
     WorkspaceLease ws(dev);
-    ws->ensure_text(avail);
-    CK(cudaEventRecord(ws->ev[0], ws->stream));
-    CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
-    const uint64_t total = run_to_completion(*dt, *ws, owned, avail, g0, &st);
+    uint64_t total;
+    const bool streamed = owned > 2 * stream_chunk_bytes() && dt->reach != UINT64_MAX;
+    if (streamed) {
+        total = stream_scan(*dt, *ws, text, avail, owned, g0, dt->reach ? dt->reach - 1 : 0, st);
+    } else {
+        ws->ensure_text(avail);
+        CK(cudaEventRecord(ws->ev[0], ws->stream));
+        CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
+        total = run_to_completion(*dt, *ws, owned, avail, g0, &st);
+        st.chunks = 1;
+    }
     out->allocate(size_t(total));
     if (total)
         CK(cudaMemcpyAsync(out->data, ws->d_out, size_t(total) * sizeof(hepfac_match_t), cudaMemcpyDeviceToHost,
                            ws->stream));
     CK(cudaEventRecord(ws->ev[3], ws->stream));
     CK(cudaStreamSynchronize(ws->stream));
-    st.h2d_ms = elapsed_ms(ws->ev[0], ws->ev[1]);
-    st.kernel_ms = elapsed_ms(ws->ev[1], ws->ev[2]);
+    st.h2d_ms = elapsed_ms(ws->ev[0], ws->ev[1]);  // streamed: first chunk only
+    st.kernel_ms = elapsed_ms(ws->ev[1], ws->ev[2]); // streamed: kernels overlapped with later copies
     st.d2h_ms = elapsed_ms(ws->ev[2], ws->ev[3]);
     st.total_ms = elapsed_ms(ws->ev[0], ws->ev[3]);
     st.matches = total;
-    st.chunks = 1;
     t_stats = st;
     return out;
 }
@@ -524,11 +620,12 @@ Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes
     std::vector<hepfac_match_t> host;
     double sum_scan = 0, sum_merge = 0;
     for (uint32_t i = 0; i < runs; ++i) {
+        ws->begin_scan();
         CK(cudaEventRecord(ws->ev[0], ws->stream));
         enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0);
         CK(cudaEventRecord(ws->ev[1], ws->stream));
         if (!fetch_small(*ws, *dt, bytes)) fail(HEPFAC_ERR_INTERNAL, "scan buffers overflowed after warm-up");
-        r.matches = ws->h_small[1];
+        r.matches = records_of(*ws);
         host.resize(size_t(r.matches));
         CK(cudaEventRecord(ws->ev[2], ws->stream));
         if (r.matches)
@@ -595,6 +692,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventCreate(&e));
         s->evs.push_back(e);
     }
+    ws.begin_scan();
     for (uint32_t i = 0; i < iterations; ++i) {
         if (flush_l2)
             gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
@@ -603,7 +701,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
     }
     s->complete = !can_match || fetch_small(ws, dt, s->owned); // grows buffers for the next run
-    s->matches = can_match ? ws.h_small[1] : 0;
+    s->matches = can_match ? records_of(ws) : 0;
     for (uint32_t i = 0; i < iterations; ++i)
         if (ms_each) ms_each[i] = elapsed_ms(s->evs[2 * i], s->evs[2 * i + 1]);
 }

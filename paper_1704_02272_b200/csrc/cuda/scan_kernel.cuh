@@ -153,8 +153,11 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 // One failure-less walk (scan.cpp:20-51).  Each step issues a single record
 // load that yields both the current node's flags (terminal / bucket) and the
 // transition for the next byte.
+// `s_txt` / `s_room`: the start's bytes that are still staged in shared
+// memory (the rest come from global memory).
 template <bool GROUPED, bool IDENT>
-__device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, Sink& sink)
+__device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, const uint8_t* s_txt,
+                                     uint32_t s_room, Sink& sink)
 {
     const TrieView& t = a.trie;
     const uint8_t* txt = a.text + start;
@@ -164,7 +167,7 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
     uint32_t node = 0, depth = 0;
     for (;;) {
         const bool more = depth < room;
-        const uint32_t byte = more ? uint32_t(__ldg(txt + depth)) : 0u;
+        const uint32_t byte = more ? (depth < s_room ? uint32_t(s_txt[depth]) : uint32_t(__ldg(txt + depth))) : 0u;
         const uint32_t sym = IDENT ? byte : uint32_t(s_sym[byte]);
         const bool step = more && (IDENT || sym != kNoSym);
         uint32_t word, base, meta, inline_id = kNoId;
@@ -292,28 +295,29 @@ template <bool GROUPED, bool IDENT>
 struct Walker {
     const ScanArgs& a;
     const uint16_t* s_sym;
-    uint16_t* q; // this warp's queue
+    uint16_t* q; // this warp's queue: survivor offsets inside the current group
     uint32_t lane;
     hepfac_match_t* region;
     uint64_t cursor; // records this warp has staged so far
 
-    // Walk queue entries [0, n) of the tile starting at `lo`; append their
-    // records in order; return how many were produced.
-    __device__ __forceinline__ uint32_t drain(uint64_t lo, uint32_t n)
+    // Walk queue entries [0, n) of the group whose text starts at global
+    // offset `gbase` and is staged at `stage` (`slen` bytes); append their
+    // records in order.
+    __device__ __forceinline__ void drain(uint64_t gbase, const uint8_t* stage, uint32_t slen, uint32_t n)
     {
-        uint32_t produced = 0;
         for (uint32_t r0 = 0; r0 < n; r0 += 32) {
             const uint32_t e = r0 + lane;
             Sink sink;
             uint64_t start = 0;
             if (e < n) {
-                start = lo + q[e];
-                walk<GROUPED, IDENT>(a, s_sym, start, sink);
+                const uint32_t o = q[e];
+                start = gbase + o;
+                walk<GROUPED, IDENT>(a, s_sym, start, stage + o, slen - o, sink);
             }
             uint32_t tot;
             const uint32_t ex = warp_exclusive(sink.n, lane, tot);
             if (sink.n) {
-                const uint64_t at = cursor + produced + ex;
+                const uint64_t at = cursor + ex;
                 uint4* dst = reinterpret_cast<uint4*>(region);
                 if (at < a.warp_cap) dst[at] = sink.r0;
                 if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
@@ -323,13 +327,11 @@ struct Walker {
                     wr.at = at + kRegRecords;
                     wr.cap = a.warp_cap;
                     wr.skip = kRegRecords;
-                    walk<GROUPED, IDENT>(a, s_sym, start, wr);
+                    walk<GROUPED, IDENT>(a, s_sym, start, nullptr, 0, wr);
                 }
             }
-            produced += tot;
+            cursor += tot;
         }
-        cursor += produced; // later drains of the same tile append after these
-        return produced;
     }
 };
 
@@ -347,7 +349,8 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar)
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // The stage's previous contents were consumed into registers before the
+    // warp's __syncwarp, so the copy cannot overwrite data still being read.
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
     asm volatile(
@@ -392,23 +395,20 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint8_t* ring = s_ring + warp * kStages * kStageBytes;
     uint64_t* bars = s_bar[warp];
 
-    // Producer (lane 0): walks the warp's group sequence -- tile gw, gw + W,
-    // ...; 16 groups each -- and keeps kStages groups in flight.  Groups past
-    // the text end are skipped by producer and consumer alike, so both sides
-    // see the same stage order.
-    uint64_t p_tile = gw;
+    // Producer (lane 0): walks the warp's group sequence -- tiles gw, gw + W,
+    // ..., 16 groups each, up to `stop` -- keeping kStages groups in flight.
+    // The consumer below visits exactly the same groups in the same order.
+    const uint64_t stop = min(avail16, a.n_tiles * uint64_t(kTile));
+    uint64_t p_addr = uint64_t(gw) * kTile;
     uint32_t p_g = 0, p_stage = 0;
+    const uint64_t p_skip = uint64_t(W - 1) * kTile;
     auto produce = [&]() {
-        for (;;) {
-            if (p_tile >= a.n_tiles) return;
-            const uint64_t p = p_tile * kTile + p_g * kGroup;
-            if (++p_g == kGroupsPerTile) p_g = 0, p_tile += W;
-            if (p >= avail16) continue;
-            const uint32_t n = uint32_t(min(uint64_t(kStageBytes), avail16 - p));
-            bulk_load(ring + p_stage * kStageBytes, a.text + p, n, &bars[p_stage]);
-            p_stage = p_stage + 1 == kStages ? 0u : p_stage + 1;
-            return;
-        }
+        if (p_addr >= stop) return;
+        const uint32_t n = uint32_t(min(uint64_t(kStageBytes), avail16 - p_addr));
+        bulk_load(ring + p_stage * kStageBytes, a.text + p_addr, n, &bars[p_stage]);
+        p_stage = p_stage + 1 == kStages ? 0u : p_stage + 1;
+        p_addr += kGroup;
+        if (++p_g == kGroupsPerTile) p_g = 0, p_addr += p_skip;
     };
     if (lane == 0) {
         for (uint32_t s = 0; s < kStages; ++s) mbar_init(&bars[s]);
@@ -419,47 +419,37 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
 
     Walker<GROUPED, IDENT> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
     uint32_t c_stage = 0, c_parity = 0;
-    const uint8_t* my_bytes = ring + lane * kLaneStarts;
     for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
         const uint64_t lo = tile * kTile;
         const uint64_t slot = wk.cursor;
         // tile-relative limits (32-bit): starts that may report, groups fetched
         const uint32_t rem = start_end > lo ? uint32_t(min(start_end - lo, uint64_t(kTile))) : 0u;
-        const uint32_t fetched = lo < avail16 ? uint32_t(min((avail16 - lo + kGroup - 1) / kGroup,
-                                                             uint64_t(kGroupsPerTile)))
-                                              : 0u;
-        uint32_t qn = 0;
+        const uint32_t fetched = uint32_t(min((stop - lo + kGroup - 1) / kGroup, uint64_t(kGroupsPerTile)));
         for (uint32_t g = 0; g < fetched; ++g) {
             const int32_t r = int32_t(rem) - int32_t(g * kGroup + lane * kLaneStarts);
             const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            const uint8_t* stage = ring + c_stage * kStageBytes;
             mbar_wait(&bars[c_stage], c_parity);
             uint32_t mask = 0;
             if (__any_sync(0xFFFFFFFFu, valid)) {
-                const uint8_t* src = my_bytes + c_stage * kStageBytes;
+                const uint8_t* src = stage + lane * kLaneStarts;
                 const uint4 v = *reinterpret_cast<const uint4*>(src);
                 const uint2 x = *reinterpret_cast<const uint2*>(src + 16);
                 const uint32_t w[6] = {v.x, v.y, v.z, v.w, x.x, x.y};
                 mask = filter_mask<KW>(t, w, s_filter, valid);
             }
+            if (__any_sync(0xFFFFFFFFu, mask)) { // compact + walk while the text is staged
+                uint32_t tot;
+                uint32_t at = warp_exclusive(__popc(mask), lane, tot);
+                for (uint32_t m = mask; m; m &= m - 1) wk.q[at++] = uint16_t(lane * kLaneStarts + __ffs(m) - 1);
+                __syncwarp();
+                const uint64_t gbase = lo + g * kGroup;
+                wk.drain(gbase, stage, uint32_t(min(uint64_t(kStageBytes), avail16 - gbase)), tot);
+            }
             __syncwarp();
             if (lane == 0) produce(); // refill the stage just consumed
             if (++c_stage == kStages) c_stage = 0, c_parity ^= 1u;
-
-            uint32_t tot;
-            const uint32_t ex = warp_exclusive(__popc(mask), lane, tot);
-            if (qn + tot > kQueue) { // warp-uniform: flush the queue first
-                wk.drain(lo, qn);
-                qn = 0;
-                __syncwarp();
-            }
-            uint32_t at = qn + ex;
-            for (uint32_t m = mask; m; m &= m - 1)
-                wk.q[at++] = uint16_t(g * kGroup + lane * kLaneStarts + __ffs(m) - 1);
-            qn += tot;
-            __syncwarp();
         }
-        wk.drain(lo, qn);
-        __syncwarp();
         if (lane == 0) {
             a.tile_count[tile] = uint32_t(wk.cursor - slot);
             a.tile_slot[tile] = uint32_t(slot);

@@ -270,3 +270,30 @@ def test_foreign_terminal_is_reported(gpu, tmp_path):
         gpu.scan(bad, b"xxAByy")
     assert e.value.status == H.INTERNAL and "spells no dictionary pattern" in e.value.message
     assert gpu.scan(bad, b"xxXYZWyy").size == 1
+
+
+@pytest.mark.parametrize("sigma,stages,depth", [(256, 2, None), (4, 1, 5), (256, 0, 3)])
+def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth):
+    # hepfac_scan streams texts longer than two chunks (H2D of chunk c+1 under
+    # the kernel of chunk c, device-side running output base); 1 MiB chunks
+    # force many chunk seams, planted matches straddle them.
+    rng = np.random.default_rng(sigma + 7)
+    a, syms = alphabet_bytes(gpu, sigma)
+    pats = pattern_set(rng, syms, 300, 4, 40)
+    tx = text(rng, syms, 5 * (1 << 20) + 12345)
+    for c in range(1 << 20, tx.size, 1 << 20):
+        for i in range(6):
+            p = pats[int(rng.integers(0, len(pats)))]
+            plant(tx, p, c - len(p) + 1 + i * 3)
+    for i in range(0, tx.size - 64, 4099):
+        plant(tx, pats[i % len(pats)], i)
+    t = build(gpu, pats, sigma, stages, depth)
+    want = oracle.naive_find_all(tx, pats)
+    monkeypatch.setenv("HEPFAC_CHUNK_MIB", "1")
+    got = gpu.scan(t, tx)
+    st = gpu.last_scan_stats()
+    assert st["chunks"] == 6
+    assert same(got, want)
+    monkeypatch.setenv("HEPFAC_CHUNK_MIB", "64")
+    assert same(gpu.scan(t, tx), want)
+    assert gpu.last_scan_stats()["chunks"] == 1
