@@ -191,8 +191,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.min_emit = im.min_emit;
 
     d->kernel = select_kernel(d->grouped, d->identity, d->kw);
-    d->smem = size_t(gpu::kWarps) * gpu::kStages * gpu::kStageBytes + size_t(gpu::kWarps) * gpu::kQueue * 2 + 512 +
-              size_t(v.filter_words) * 4;
+    d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes();
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);

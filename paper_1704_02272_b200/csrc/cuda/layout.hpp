@@ -31,9 +31,10 @@ constexpr uint32_t kNoId = 0xFFFFFFFFu;
 constexpr uint16_t kNoSym = 0xFFFFu;
 constexpr uint32_t kMaxFilterKey = 8; // bytes hashed by the start filter
 
-// Rolling hash of a byte string (1-based bytes so 0x00 counts), mixed with
-// the length: the dictionary key of a matched slice.
-HFB_HD uint64_t slice_step(uint64_t h, uint64_t mul, uint32_t byte) { return h * mul + byte + 1; }
+// Dictionary key of a matched slice: the slice read as little-endian 32-bit
+// words (the last one zero-padded), folded with an odd multiplier, mixed with
+// the length.  Word-wise so the GPU hashes 4 bytes per step.
+HFB_HD uint64_t slice_step(uint64_t h, uint64_t mul, uint32_t word) { return (h + word + 1) * mul; }
 HFB_HD uint64_t slice_key(uint64_t h, uint32_t len) { return h ^ (uint64_t(len) * 0x9E3779B97F4A7C15ull); }
 HFB_HD uint64_t mix64(uint64_t k)
 {
@@ -45,19 +46,17 @@ HFB_HD uint64_t mix64(uint64_t k)
     return k;
 }
 
-// Start filter: the first k text bytes (little-endian packed) hashed to a
-// 2^bits bitmap.  k <= 4 uses a 32-bit multiply, k <= 8 a 64-bit one.
-HFB_HD uint32_t filter_slot32(uint32_t key, uint32_t bits) { return (key * 0x9E3779B1u) >> (32 - bits); }
-HFB_HD uint32_t filter_slot64(uint64_t key, uint32_t bits)
+// Start filter: the first k text bytes (little-endian packed into a 64-bit
+// key) are folded to 32 bits; the bitmap word comes from a multiplicative
+// hash of the folded key, the bit inside the word from its low 5 bits (the
+// first byte).  Bits are stored MSB-first, so the kernel brings a bit to the
+// top with one wrapping funnel shift by the key itself.
+HFB_HD uint32_t filter_fold(uint64_t key)
 {
-    return uint32_t((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+    return uint32_t(key) ^ (uint32_t(key >> 32) * 0x85EBCA77u);
 }
-// Second, independent probe (Bloom filter with two hash functions).
-HFB_HD uint32_t filter_slot32b(uint32_t key, uint32_t bits) { return ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - bits); }
-HFB_HD uint32_t filter_slot64b(uint64_t key, uint32_t bits)
-{
-    return uint32_t(((key ^ (key >> 29)) * 0xBF58476D1CE4E5B9ull) >> (64 - bits));
-}
+HFB_HD uint32_t filter_word(uint32_t key32, uint32_t word_bits) { return (key32 * 0x9E3779B1u) >> (32 - word_bits); }
+HFB_HD uint32_t filter_mask_bit(uint32_t key32) { return 0x80000000u >> (key32 & 31u); }
 
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {

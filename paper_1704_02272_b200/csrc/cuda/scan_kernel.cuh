@@ -4,24 +4,24 @@
 // (transition).  One logical walk per text offset, as in the paper
 // (PAPER.md:87-95).
 //
-// GPU work decomposition: one cooperative, persistent launch of 1024-thread
-// CTAs (one per SM).  The only block-wide state is read-only: the start filter
-// (a Bloom bitmap over the trie's depth-k path strings) and the byte->symbol
-// map, both in shared memory.  Everything else is per warp, so no warp ever
-// waits for another during the scan itself:
+// GPU work decomposition: one cooperative, persistent launch with one CTA per
+// SM.  Block-wide state is read-only: the start filter (a bitmap over the
+// trie's depth-k path strings) and the byte->symbol map, in shared memory.
+// Everything else is per warp, so no warp ever waits for another during the
+// scan itself:
 //
-//   phase 1, per warp, over statically interleaved 8 KiB warp-tiles:
-//     - text arrives straight in registers: each lane loads 16 bytes
-//       (coalesced 512 B per warp), the next group is always in flight;
-//     - each lane probes the filter for its 16 starts (one shared-memory
-//       probe per start, a second probe only for first-probe hits);
-//     - survivors are compacted in start order into a per-warp queue in
-//       shared memory; when it fills (or the tile ends) the lanes walk the
-//       queued starts in parallel through the GPU trie image (one 8/16-byte
-//       __ldg per text byte);
-//     - a warp scan of the per-lane record counts writes the records, in
-//       order, into the warp's private staging region; the tile's count and
-//       staging offset go to a small per-tile table.
+//   phase 1, per warp, over statically interleaved 8 KiB warp-tiles
+//   (8 groups of 1 KiB: 32 lanes x 32 consecutive starts):
+//     - lane 0 keeps kStages groups in flight with cp.async.bulk (TMA bulk
+//       copies, mbarrier-tracked) into the warp's ring in shared memory;
+//     - each lane probes the filter for its 32 starts (7 SASS instructions per
+//       start: one shared-memory word load, one funnel shift to test the bit);
+//     - survivors are compacted in start order into a per-warp queue and
+//       walked right away, lane-parallel, reading text from the staged group
+//       (the trie image through __ldg: one 8/16-byte record per text byte);
+//     - a warp scan of the per-lane record counts appends the records, in
+//       order, to the warp's private staging region in HBM; per tile the
+//       record count and staging offset go to a small table.
 //   grid sync -> phase 2: per-CTA sums of the tile counts.
 //   grid sync -> phase 3: each CTA scans its contiguous range of tiles and
 //     copies their staged records to their final offsets, so the output is
@@ -40,20 +40,20 @@ namespace hfb::gpu {
 namespace cg = cooperative_groups;
 
 #ifndef HFB_WARPS
-#define HFB_WARPS 32
+#define HFB_WARPS 16
 #endif
 #ifndef HFB_STAGES
 #define HFB_STAGES 3
 #endif
 constexpr uint32_t kWarps = HFB_WARPS; // warps per CTA (one CTA per SM)
 constexpr uint32_t kThreads = kWarps * 32;
-constexpr uint32_t kLaneStarts = 16;                 // consecutive starts per lane per group
-constexpr uint32_t kGroup = 32 * kLaneStarts;         // 512 starts per warp group
-constexpr uint32_t kGroupsPerTile = 16;
+constexpr uint32_t kLaneStarts = 32;                 // consecutive starts per lane per group
+constexpr uint32_t kGroup = 32 * kLaneStarts;         // 1024 starts per warp group
+constexpr uint32_t kGroupsPerTile = 8;
 constexpr uint32_t kTile = kGroup * kGroupsPerTile;   // 8192 starts per warp-tile
-constexpr uint32_t kQueue = kGroup;                   // per-warp survivor queue (>= one group)
+constexpr uint32_t kQueue = kGroup;                   // per-warp survivor queue (one group)
 constexpr uint32_t kStages = HFB_STAGES;              // per-warp TMA ring depth (groups in flight)
-constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the 8-byte key overhang, 16-aligned
+constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the key overhang, 16-aligned
 constexpr uint32_t kRegRecords = 2;                   // records a lane keeps per walk round
 
 struct ScanArgs {
@@ -73,33 +73,42 @@ struct ScanArgs {
     unsigned long long* total;
     const unsigned long long* base_in; // records placed by earlier launches of a streamed scan
     unsigned long long* base_out;      // base_in + this launch's total (distinct word)
-    unsigned long long* warp_need; // max records any warp needed (overflow sizing)
+    unsigned long long* warp_need;     // max records any warp needed (overflow sizing)
     unsigned int* err;
 };
 
-// ---- walk --------------------------------------------------------------------
+// ---- text and dictionary helpers --------------------------------------------------
 
-__device__ __forceinline__ uint32_t text_byte(const ScanArgs& a, uint64_t pos)
+// 4 text bytes at any offset (little-endian), from two aligned word loads.
+// The text buffer is padded, so reading up to 7 bytes past n_avail is safe.
+__device__ __forceinline__ uint32_t text_word(const ScanArgs& a, uint64_t pos)
 {
-    return uint32_t(__ldg(a.text + pos));
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(a.text + (pos & ~3ull));
+    const uint32_t sh = uint32_t(pos & 3u) * 8u;
+    const uint32_t lo = __ldg(p);
+    return sh ? __funnelshift_r(lo, __ldg(p + 1), sh) : lo;
 }
 
+__device__ __forceinline__ uint32_t tail_mask(uint32_t left) { return left >= 4 ? 0xFFFFFFFFu : (1u << (8 * left)) - 1u; }
+
+// text[start, start + len) == pattern id, 4 bytes per step (patterns are
+// stored 4-byte aligned and zero padded in the image).
 __device__ __noinline__ bool same_bytes(const ScanArgs& a, uint64_t start, uint32_t id, uint32_t len)
 {
-    const uint8_t* p = a.trie.pat_bytes + __ldg(a.trie.pat_off + id);
-    for (uint32_t i = 0; i < len; ++i)
-        if (text_byte(a, start + i) != uint32_t(__ldg(p + i))) return false;
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(a.trie.pat_bytes + __ldg(a.trie.pat_off + id));
+    for (uint32_t i = 0; i < len; i += 4)
+        if ((text_word(a, start + i) ^ __ldg(p + i / 4)) & tail_mask(len - i)) return false;
     return true;
 }
 
-// Shared terminal: identify the slice by its key, then confirm byte-wise
-// (the reference's dictionary lookup, trie.hpp:103-107; a miss is its
-// logic_error "terminal node spells no dictionary pattern", scan.cpp:34).
+// Shared terminal: identify the slice by its key, then confirm it (the
+// reference's dictionary lookup, trie.hpp:103-107; a miss is its logic_error
+// "terminal node spells no dictionary pattern", scan.cpp:34).
 __device__ __noinline__ uint32_t resolve_slice(const ScanArgs& a, uint64_t start, uint32_t len)
 {
     const TrieView& t = a.trie;
-    uint64_t h = 0; // the slice key is computed only here, off the per-step path
-    for (uint32_t i = 0; i < len; ++i) h = slice_step(h, t.hmul, text_byte(a, start + i));
+    uint64_t h = 0;
+    for (uint32_t i = 0; i < len; i += 4) h = slice_step(h, t.hmul, text_word(a, start + i) & tail_mask(len - i));
     const uint64_t key = slice_key(h, len);
     for (uint64_t s = mix64(key) & t.ht_mask;; s = (s + 1) & t.ht_mask) {
         const uint32_t id = __ldg(t.ht_id + s);
@@ -152,16 +161,14 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 
 // One failure-less walk (scan.cpp:20-51).  Each step issues a single record
 // load that yields both the current node's flags (terminal / bucket) and the
-// transition for the next byte.
-// `s_txt` / `s_room`: the start's bytes that are still staged in shared
-// memory (the rest come from global memory).
+// transition for the next byte.  `s_txt` / `s_room`: the start's bytes that
+// are staged in shared memory (the rest come from global memory).
 template <bool GROUPED, bool IDENT>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, const uint8_t* s_txt,
                                      uint32_t s_room, Sink& sink)
 {
     const TrieView& t = a.trie;
     const uint8_t* txt = a.text + start;
-    // bytes this walk may consume before the text (or shard halo) ends
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
     const uint32_t limit = t.depth_limit ? t.depth_limit : 0xFFFFFFFFu;
     uint32_t node = 0, depth = 0;
@@ -185,13 +192,11 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
             base = r.y & kBaseMask;
             meta = r.y;
         }
-        if (meta & (kFlagTerminal | kFlagBucket)) {
-            if (depth && (meta & kFlagTerminal)) {
-                uint32_t id = GROUPED ? inline_id : __ldg(t.term_id + node);
-                if (id == kNoId) id = resolve_slice(a, start, depth);
-                if (id == kNoId) atomicOr(a.err, 1u);
-                else sink.put(a.g0 + start, depth, id);
-            }
+        if (depth && (meta & kFlagTerminal)) {
+            uint32_t id = GROUPED ? inline_id : __ldg(t.term_id + node);
+            if (id == kNoId) id = resolve_slice(a, start, depth);
+            if (id == kNoId) atomicOr(a.err, 1u);
+            else sink.put(a.g0 + start, depth, id);
         }
         if (depth == limit) { // depth-limit nodes are leaves (scan.cpp:37-49)
             if (meta & kFlagBucket) verify_bucket(a, node, start, sink);
@@ -207,51 +212,35 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
 
 // ---- start filter ------------------------------------------------------------
 
-// Bitmap bits are stored MSB-first inside each word (bit slot s lives at
-// position 31 - (s & 31)), so a probe is: load the word, shift the wanted bit
-// to the top with a wrapping funnel shift, and funnel it into the mask.
-__device__ __forceinline__ uint32_t probe_into(uint32_t m, const uint32_t* s_filter, uint32_t slot)
-{
-    const uint32_t w = s_filter[slot >> 5];
-    return __funnelshift_l(__funnelshift_l(0u, w, slot), m, 1); // (m << 1) | bit
-}
-
-// Bit j set = start j of this lane's 16 may report.
+// Bit j set = start j of this lane's 32 may report.  w[0..9] = the lane's
+// 32 bytes plus the next 8.  KW: 1 = k < 4, 2 = k in 5..8, 3 = k == 4.
 template <int KW>
-__device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_t (&w)[6], const uint32_t* s_filter,
+__device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_t (&w)[10], const uint32_t* s_filter,
                                                 uint32_t valid)
 {
     if (KW == 0) return valid;
-    const uint32_t k = t.filter_k, bits = t.filter_bits;
-    // KW: 1 = k < 4 (masked 32-bit key), 2 = 5..8 bytes (64-bit key), 3 = exactly 4 bytes
+    const uint32_t k = t.filter_k;
+    const uint32_t shift = 30u - (t.filter_bits - 5u); // hash -> byte offset of the bitmap word
     const uint32_t m32 = (KW == 3 || k >= 4) ? 0xFFFFFFFFu : ((1u << (8 * k)) - 1u);
     const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
-    auto key32 = [&](int j) {
-        const uint32_t x = (j & 3) ? __funnelshift_r(w[j >> 2], w[(j >> 2) + 1], 8 * (j & 3)) : w[j >> 2];
-        return KW == 3 ? x : (x & m32);
-    };
-    auto key64 = [&](int j) {
+    const uint8_t* fbytes = reinterpret_cast<const uint8_t*>(s_filter);
+    uint32_t m = 0; // start j ends up at bit 31 - j
+#pragma unroll
+    for (int j = 0; j < int(kLaneStarts); ++j) {
         const uint32_t lo = (j & 3) ? __funnelshift_r(w[j >> 2], w[(j >> 2) + 1], 8 * (j & 3)) : w[j >> 2];
-        const uint32_t hi =
-            ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
-        return (uint64_t(hi) << 32) | lo;
-    };
-    uint32_t m = 0; // start j ends up at bit 15 - j
-#pragma unroll
-    for (int j = 0; j < int(kLaneStarts); ++j)
-        m = probe_into(m, s_filter, KW != 2 ? filter_slot32(key32(j), bits) : filter_slot64(key64(j), bits));
-    m = (__brev(m) >> 16) & valid; // start j at bit j
-    if (m && t.filter_hashes > 1) {
-        uint32_t m2 = 0;
-#pragma unroll
-        for (int j = 0; j < int(kLaneStarts); ++j) {
-            const uint32_t slot = KW != 2 ? filter_slot32b(key32(j), bits) : filter_slot64b(key64(j), bits);
-            const uint32_t w2 = (m >> j) & 1u ? s_filter[slot >> 5] : 0u;
-            m2 |= (__funnelshift_l(0u, w2, slot) >> 31) << j;
+        uint32_t key;
+        if (KW == 2) {
+            const uint32_t hi =
+                ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
+            key = lo ^ (hi * 0x85EBCA77u); // filter_fold
+        } else {
+            key = KW == 3 ? lo : (lo & m32);
         }
-        m = m2;
+        const uint32_t off = ((key * 0x9E3779B1u) >> shift) & ~3u; // filter_word(key) * 4
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(fbytes + off);
+        m = __funnelshift_l(__funnelshift_l(0u, word, key), m, 1); // (m << 1) | bit (key & 31), MSB-first
     }
-    return m;
+    return __brev(m) & valid; // start j at bit j
 }
 
 // ---- warp helpers ---------------------------------------------------------------
@@ -289,7 +278,7 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
     return r;
 }
 
-// ---- the kernel ----------------------------------------------------------------
+// ---- the walk stage of one warp ---------------------------------------------------
 
 template <bool GROUPED, bool IDENT>
 struct Walker {
@@ -349,8 +338,8 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar)
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 {
-    // The stage's previous contents were consumed into registers before the
-    // warp's __syncwarp, so the copy cannot overwrite data still being read.
+    // The stage's previous contents were consumed before the warp's
+    // __syncwarp, so the copy cannot overwrite data still being read.
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
     asm volatile(
@@ -370,15 +359,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
+// Shared-memory bytes a CTA needs beyond the filter bitmap.
+constexpr uint32_t smem_fixed_bytes() { return kWarps * kStages * kStageBytes + kWarps * kQueue * 2 + 512; }
+
 template <bool GROUPED, bool IDENT, int KW>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t fwords = KW ? a.trie.filter_words : 0u;
-    uint8_t* s_ring = smem;                                                     // [warp][stage][kStageBytes]
-    uint16_t* s_queue = reinterpret_cast<uint16_t*>(smem + kWarps * kStages * kStageBytes);
-    uint16_t* s_sym = s_queue + kWarps * kQueue;                                // [256]
-    uint32_t* s_filter = reinterpret_cast<uint32_t*>(s_sym + 256);
+    uint32_t* s_filter = reinterpret_cast<uint32_t*>(smem);                   // first: 2^bits / 8 bytes
+    uint8_t* s_ring = smem + size_t(fwords) * 4;                               // [warp][stage][kStageBytes]
+    uint16_t* s_queue = reinterpret_cast<uint16_t*>(s_ring + kWarps * kStages * kStageBytes);
+    uint16_t* s_sym = s_queue + kWarps * kQueue;                               // [256]
     __shared__ uint64_t s_bar[kWarps][kStages];
     __shared__ uint32_t s_scr[kWarps + 1];
 
@@ -395,9 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     uint8_t* ring = s_ring + warp * kStages * kStageBytes;
     uint64_t* bars = s_bar[warp];
 
-    // Producer (lane 0): walks the warp's group sequence -- tiles gw, gw + W,
-    // ..., 16 groups each, up to `stop` -- keeping kStages groups in flight.
-    // The consumer below visits exactly the same groups in the same order.
+    // Producer (lane 0): the warp's groups -- tiles gw, gw + W, ..., 8 groups
+    // each, up to `stop` -- with kStages in flight.  The consumer below visits
+    // exactly the same groups in the same order.
     const uint64_t stop = min(avail16, a.n_tiles * uint64_t(kTile));
     uint64_t p_addr = uint64_t(gw) * kTile;
     uint32_t p_g = 0, p_stage = 0;
@@ -427,15 +419,16 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint32_t fetched = uint32_t(min((stop - lo + kGroup - 1) / kGroup, uint64_t(kGroupsPerTile)));
         for (uint32_t g = 0; g < fetched; ++g) {
             const int32_t r = int32_t(rem) - int32_t(g * kGroup + lane * kLaneStarts);
-            const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
             const uint8_t* stage = ring + c_stage * kStageBytes;
             mbar_wait(&bars[c_stage], c_parity);
             uint32_t mask = 0;
             if (__any_sync(0xFFFFFFFFu, valid)) {
                 const uint8_t* src = stage + lane * kLaneStarts;
-                const uint4 v = *reinterpret_cast<const uint4*>(src);
-                const uint2 x = *reinterpret_cast<const uint2*>(src + 16);
-                const uint32_t w[6] = {v.x, v.y, v.z, v.w, x.x, x.y};
+                const uint4 v0 = *reinterpret_cast<const uint4*>(src);
+                const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
+                const uint2 x = *reinterpret_cast<const uint2*>(src + 32);
+                const uint32_t w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, x.x, x.y};
                 mask = filter_mask<KW>(t, w, s_filter, valid);
             }
             if (__any_sync(0xFFFFFFFFu, mask)) { // compact + walk while the text is staged

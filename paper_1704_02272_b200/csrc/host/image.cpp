@@ -87,11 +87,12 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     im.pat_off.resize(P);
     im.pat_len.resize(P);
     for (size_t i = 0; i < P; ++i) {
-        im.pat_off[i] = im.pat_bytes.size();
+        im.pat_off[i] = im.pat_bytes.size(); // 4-byte aligned, zero padded: word compares
         im.pat_len[i] = uint32_t(t.patterns[i].size());
         im.pat_bytes.insert(im.pat_bytes.end(), t.patterns[i].begin(), t.patterns[i].end());
+        im.pat_bytes.resize((im.pat_bytes.size() + 3) & ~size_t(3), 0);
     }
-    if (im.pat_bytes.empty()) im.pat_bytes.push_back(0);
+    im.pat_bytes.resize(im.pat_bytes.size() + 8, 0); // word reads may overrun the last pattern
     std::vector<uint64_t> keys(P);
     for (uint64_t attempt = 0;; ++attempt) {
         im.hmul = 0x100000001B3ull + 2 * attempt * 0x9E3779B97F4A7C15ull; // odd multipliers
@@ -99,9 +100,14 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         seen.reserve(P * 2);
         bool unique = true;
         for (size_t i = 0; i < P && unique; ++i) {
+            const std::string& p = t.patterns[i];
             uint64_t h = 0;
-            for (unsigned char c : t.patterns[i]) h = slice_step(h, im.hmul, c);
-            keys[i] = slice_key(h, uint32_t(t.patterns[i].size()));
+            for (size_t o = 0; o < p.size(); o += 4) {
+                uint32_t w = 0;
+                for (size_t b = 0; b < 4 && o + b < p.size(); ++b) w |= uint32_t(uint8_t(p[o + b])) << (8 * b);
+                h = slice_step(h, im.hmul, w);
+            }
+            keys[i] = slice_key(h, uint32_t(p.size()));
             unique = seen.insert(keys[i]).second;
         }
         if (unique) break;
@@ -281,15 +287,11 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             const uint32_t bits =
                 std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, opt.max_filter_bits);
             im.filter_bits = bits;
-            im.filter_hashes = opt.filter_hashes;
+            im.filter_hashes = 1;
             im.filter.assign((size_t(1) << bits) / 32, 0u);
             for (uint64_t g : grams) {
-                const uint32_t s = k <= 4 ? filter_slot32(uint32_t(g), bits) : filter_slot64(g, bits);
-                im.filter[s >> 5] |= 0x80000000u >> (s & 31); // MSB-first (probe_into)
-                if (im.filter_hashes > 1) {
-                    const uint32_t s2 = k <= 4 ? filter_slot32b(uint32_t(g), bits) : filter_slot64b(g, bits);
-                    im.filter[s2 >> 5] |= 0x80000000u >> (s2 & 31);
-                }
+                const uint32_t k32 = filter_fold(g);
+                im.filter[filter_word(k32, bits - 5)] |= filter_mask_bit(k32);
             }
         }
     }
