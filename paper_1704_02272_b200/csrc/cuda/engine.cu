@@ -296,11 +296,12 @@ struct Workspace {
         slot_cap = c0;
     }
     void ensure_out(uint64_t n) { regrow(d_out, out_cap, std::max<uint64_t>(n, 1)); }
+    // warp_cap only grows on overflow; the buffer covers warps * warp_cap
+    // (never derive warp_cap from the buffer size: grids differ per launch).
     void ensure_stage(uint64_t warps, uint64_t per_warp)
     {
         warp_cap = std::max(warp_cap, per_warp);
         regrow(d_stage, stage_cap, warps * warp_cap);
-        warp_cap = stage_cap / warps; // a bigger region from an earlier grid is reused
     }
     void ensure_tiles(uint64_t tiles, uint64_t grid)
     {
