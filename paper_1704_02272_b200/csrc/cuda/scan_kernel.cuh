@@ -40,10 +40,10 @@ namespace hfb::gpu {
 namespace cg = cooperative_groups;
 
 #ifndef HFB_WARPS
-#define HFB_WARPS 16
+#define HFB_WARPS 20
 #endif
 #ifndef HFB_STAGES
-#define HFB_STAGES 3
+#define HFB_STAGES 2
 #endif
 constexpr uint32_t kWarps = HFB_WARPS; // warps per CTA (one CTA per SM)
 constexpr uint32_t kThreads = kWarps * 32;
