@@ -165,14 +165,18 @@ def measured_hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config_name: str):
-    """dram bytes per launch from the committed ncu capture, if any."""
+def ncu_traffic(config_name: str, text_bytes: int):
+    """DRAM bytes (read + write) per launch from the committed ncu --set full
+    capture of this workload (profiles/ncu_traffic.json), scaled to this
+    launch's text size when the capture used a smaller text; None if absent."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(config_name)
-    return None
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f).get(config_name)
+    if not d:
+        return None
+    return int(round(d["dram_bytes"] * text_bytes / d["text_bytes"]))
 
 
 def make_shard(w, rank: int, world: int, per_gpu: int, halo: int):
@@ -326,7 +330,7 @@ def main():
     alg_bytes = owned + 16 * int(matches)
     achieved = alg_bytes / mean_launch_s / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config, owned),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "per_unit": "1 B text read per start + 16 B per match written"}
