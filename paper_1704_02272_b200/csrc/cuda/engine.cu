@@ -181,13 +181,14 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.ht_id = d->upload(im.ht_id);
     v.ht_mask = im.ht_mask;
     v.hmul = im.hmul;
-    v.bk_start = d->upload(im.bk_start);
-    v.bk_ids = d->upload(im.bk_ids);
+    v.bk_span = d->upload(im.bk_span);
+    v.bk_entry = d->upload(im.bk_entry);
     v.filter = d->upload(im.filter);
     v.filter_words = d->kw ? uint32_t(im.filter.size()) : 0u;
     v.filter_bits = im.filter_bits;
     v.filter_k = im.filter_k;
-    v.filter_hashes = im.filter_hashes;
+    v.filter2 = d->upload(im.filter2);
+    v.filter2_bits = im.filter2_bits;
     v.min_emit = im.min_emit;
 
     d->kernel = select_kernel(d->grouped, d->identity, d->kw);

@@ -58,6 +58,19 @@ HFB_HD uint32_t filter_fold(uint64_t key)
 HFB_HD uint32_t filter_word(uint32_t key32, uint32_t word_bits) { return (key32 * 0x9E3779B1u) >> (32 - word_bits); }
 HFB_HD uint32_t filter_mask_bit(uint32_t key32) { return 0x80000000u >> (key32 & 31u); }
 
+// Second-level filter (global memory, L2-resident): an independent mixing hash
+// of the same folded key into a larger bitmap.  Only first-level survivors
+// (about 2%) probe it.
+HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits)
+{
+    x ^= x >> 16;
+    x *= 0x7FEB352Du;
+    x ^= x >> 15;
+    x *= 0x846CA68Bu;
+    x ^= x >> 16;
+    return x >> (32 - bits);
+}
+
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {
     const uint32_t* nodes;
@@ -73,13 +86,14 @@ struct TrieView {
     const uint32_t* ht_id;
     uint64_t ht_mask;
     uint64_t hmul;
-    const uint32_t* bk_start;
-    const uint32_t* bk_ids;
+    const uint32_t* bk_span;  // uint2 per bucket: {first entry, entry count}
+    const uint32_t* bk_entry; // uint4 {pattern id, length, byte offset lo, hi}, sorted by (length, id)
     const uint32_t* filter;
     uint32_t filter_words;
     uint32_t filter_bits; // 0 = filter disabled (every start walks)
     uint32_t filter_k;
-    uint32_t filter_hashes; // 1 or 2 probes
+    const uint32_t* filter2; // second level, 2^filter2_bits bits
+    uint32_t filter2_bits;   // 0 = no second level
     uint32_t min_emit;
 };
 

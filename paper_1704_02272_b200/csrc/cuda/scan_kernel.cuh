@@ -51,7 +51,7 @@ constexpr uint32_t kLaneStarts = 32;                 // consecutive starts per l
 constexpr uint32_t kGroup = 32 * kLaneStarts;         // 1024 starts per warp group
 constexpr uint32_t kGroupsPerTile = 8;
 constexpr uint32_t kTile = kGroup * kGroupsPerTile;   // 8192 starts per warp-tile
-constexpr uint32_t kQueue = kGroup;                   // per-warp survivor queue (one group)
+constexpr uint32_t kQueue = kGroup;                   // per-warp candidate queue (tile offsets)
 constexpr uint32_t kStages = HFB_STAGES;              // per-warp TMA ring depth (groups in flight)
 constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the key overhang, 16-aligned
 constexpr uint32_t kRegRecords = 2;                   // records a lane keeps per walk round
@@ -145,17 +145,26 @@ struct Sink {
     }
 };
 
-// Depth-limit verification (scan.cpp:37-49): bucket ids are pre-sorted by
-// (length, id), which is the order the records must appear in.
+// text[start, start + len) == the pattern stored at byte offset `off`.
+__device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint64_t off, uint32_t len)
+{
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(a.trie.pat_bytes + off);
+    for (uint32_t i = 0; i < len; i += 4)
+        if ((text_word(a, start + i) ^ __ldg(p + i / 4)) & tail_mask(len - i)) return false;
+    return true;
+}
+
+// Depth-limit verification (scan.cpp:37-49): bucket entries are pre-sorted by
+// (length, id), which is the order the records must appear in.  One load
+// gives the bucket's span, one load per entry its id, length and bytes.
 __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, Sink& sink)
 {
     const TrieView& t = a.trie;
-    const uint32_t b = __ldg(t.bucket_of + node);
-    for (uint32_t k = __ldg(t.bk_start + b), e = __ldg(t.bk_start + b + 1); k < e; ++k) {
-        const uint32_t id = __ldg(t.bk_ids + k);
-        const uint32_t len = __ldg(t.pat_len + id);
-        if (start + len > a.n_avail) continue; // overhangs the text end (scan.cpp:43)
-        if (same_bytes(a, start, id, len)) sink.put(a.g0 + start, len, id);
+    const uint2 span = __ldg(reinterpret_cast<const uint2*>(t.bk_span) + __ldg(t.bucket_of + node));
+    for (uint32_t k = span.x, e = span.x + span.y; k < e; ++k) {
+        const uint4 en = __ldg(reinterpret_cast<const uint4*>(t.bk_entry) + k);
+        if (start + en.y > a.n_avail) continue; // overhangs the text end (scan.cpp:43)
+        if (same_at(a, start, (uint64_t(en.w) << 32) | en.z, en.y)) sink.put(a.g0 + start, en.y, en.x);
     }
 }
 
@@ -280,28 +289,61 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
 
 // ---- the walk stage of one warp ---------------------------------------------------
 
-template <bool GROUPED, bool IDENT>
+// Second-level filter probe of the start at global offset `start` (text read
+// back from L2, where the TMA copy just streamed it).
+template <int KW>
+__device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
+{
+    const TrieView& t = a.trie;
+    const uint32_t k = t.filter_k;
+    uint32_t key = text_word(a, start);
+    if (KW == 1) key &= (1u << (8 * k)) - 1u;
+    if (KW == 2) {
+        const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u);
+        key ^= (text_word(a, start + 4) & mhi) * 0x85EBCA77u; // filter_fold
+    }
+    const uint32_t slot = filter2_slot(key, t.filter2_bits);
+    return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
+}
+
+template <bool GROUPED, bool IDENT, int KW>
 struct Walker {
     const ScanArgs& a;
     const uint16_t* s_sym;
-    uint16_t* q; // this warp's queue: survivor offsets inside the current group
+    uint16_t* q; // this warp's candidate queue: start offsets inside the current tile
     uint32_t lane;
     hepfac_match_t* region;
     uint64_t cursor; // records this warp has staged so far
 
-    // Walk queue entries [0, n) of the group whose text starts at global
-    // offset `gbase` and is staged at `stage` (`slen` bytes); append their
-    // records in order.
-    __device__ __forceinline__ void drain(uint64_t gbase, const uint8_t* stage, uint32_t slen, uint32_t n)
+    // Candidates [0, n) of the tile starting at `lo`: second-level probe,
+    // then walk the survivors and append their records in start order.
+    __device__ __forceinline__ void flush(uint64_t lo, uint32_t n)
     {
-        for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+        uint32_t ns = n;
+        if (KW != 0 && a.trie.filter2_bits) {
+            ns = 0;
+            const uint32_t below = (1u << lane) - 1u;
+            for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+                const uint32_t e = r0 + lane;
+                uint16_t off = 0;
+                bool keep = false;
+                if (e < n) {
+                    off = q[e];
+                    keep = probe2<KW>(a, lo + off);
+                }
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, keep); // every read of this round is done
+                if (keep) q[ns + __popc(b & below)] = off;          // compaction in place, order kept
+                ns += __popc(b);
+            }
+            __syncwarp();
+        }
+        for (uint32_t r0 = 0; r0 < ns; r0 += 32) {
             const uint32_t e = r0 + lane;
             Sink sink;
             uint64_t start = 0;
-            if (e < n) {
-                const uint32_t o = q[e];
-                start = gbase + o;
-                walk<GROUPED, IDENT>(a, s_sym, start, stage + o, slen - o, sink);
+            if (e < ns) {
+                start = lo + q[e];
+                walk<GROUPED, IDENT>(a, s_sym, start, nullptr, 0, sink);
             }
             uint32_t tot;
             const uint32_t ex = warp_exclusive(sink.n, lane, tot);
@@ -321,6 +363,7 @@ struct Walker {
             }
             cursor += tot;
         }
+        __syncwarp();
     }
 };
 
@@ -409,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     }
     __syncthreads(); // filter, symbol map and barrier inits visible
 
-    Walker<GROUPED, IDENT> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
+    Walker<GROUPED, IDENT, KW> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
     uint32_t c_stage = 0, c_parity = 0;
     for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
         const uint64_t lo = tile * kTile;
@@ -417,32 +460,38 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         // tile-relative limits (32-bit): starts that may report, groups fetched
         const uint32_t rem = start_end > lo ? uint32_t(min(start_end - lo, uint64_t(kTile))) : 0u;
         const uint32_t fetched = uint32_t(min((stop - lo + kGroup - 1) / kGroup, uint64_t(kGroupsPerTile)));
+        uint32_t qn = 0;
         for (uint32_t g = 0; g < fetched; ++g) {
             const int32_t r = int32_t(rem) - int32_t(g * kGroup + lane * kLaneStarts);
             const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
-            const uint8_t* stage = ring + c_stage * kStageBytes;
             mbar_wait(&bars[c_stage], c_parity);
             uint32_t mask = 0;
             if (__any_sync(0xFFFFFFFFu, valid)) {
-                const uint8_t* src = stage + lane * kLaneStarts;
+                const uint8_t* src = ring + c_stage * kStageBytes + lane * kLaneStarts;
                 const uint4 v0 = *reinterpret_cast<const uint4*>(src);
                 const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
                 const uint2 x = *reinterpret_cast<const uint2*>(src + 32);
                 const uint32_t w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, x.x, x.y};
                 mask = filter_mask<KW>(t, w, s_filter, valid);
             }
-            if (__any_sync(0xFFFFFFFFu, mask)) { // compact + walk while the text is staged
-                uint32_t tot;
-                uint32_t at = warp_exclusive(__popc(mask), lane, tot);
-                for (uint32_t m = mask; m; m &= m - 1) wk.q[at++] = uint16_t(lane * kLaneStarts + __ffs(m) - 1);
-                __syncwarp();
-                const uint64_t gbase = lo + g * kGroup;
-                wk.drain(gbase, stage, uint32_t(min(uint64_t(kStageBytes), avail16 - gbase)), tot);
-            }
             __syncwarp();
-            if (lane == 0) produce(); // refill the stage just consumed
+            if (lane == 0) produce(); // the stage is consumed: refill it
             if (++c_stage == kStages) c_stage = 0, c_parity ^= 1u;
+            if (__any_sync(0xFFFFFFFFu, mask)) { // queue the candidates, in start order
+                uint32_t tot;
+                const uint32_t ex = warp_exclusive(__popc(mask), lane, tot);
+                if (qn + tot > kQueue) { // warp-uniform
+                    wk.flush(lo, qn);
+                    qn = 0;
+                }
+                uint32_t at = qn + ex;
+                for (uint32_t m = mask; m; m &= m - 1)
+                    wk.q[at++] = uint16_t(g * kGroup + lane * kLaneStarts + __ffs(m) - 1);
+                qn += tot;
+                __syncwarp();
+            }
         }
+        if (qn) wk.flush(lo, qn);
         if (lane == 0) {
             a.tile_count[tile] = uint32_t(wk.cursor - slot);
             a.tile_slot[tile] = uint32_t(slot);

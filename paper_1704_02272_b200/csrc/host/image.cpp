@@ -26,7 +26,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_start.size() * 4 + bk_ids.size() * 4 + filter.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -40,9 +40,9 @@ ImageOptions image_options_from_env()
         long v = std::strtol(s, nullptr, 10);
         if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
     }
-    if (const char* s = std::getenv("HEPFAC_FILTER_HASHES")) {
+    if (const char* s = std::getenv("HEPFAC_FILTER2_SLACK")) {
         long v = std::strtol(s, nullptr, 10);
-        if (v == 1 || v == 2) o.filter_hashes = uint32_t(v);
+        if (v >= 0 && v <= 16) o.filter2_slack = uint32_t(v);
     }
     return o;
 }
@@ -155,18 +155,24 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
 
     // ---- buckets: CSR, each sorted by (length, id) -----------------------
     im.bucket_of.assign(n, kNoId);
-    im.bk_start.push_back(0);
     for (const auto& [node, ids] : t.buckets) {
         if (node >= n) continue;
-        im.bucket_of[node] = uint32_t(im.bk_start.size() - 1);
+        im.bucket_of[node] = uint32_t(im.bk_span.size() / 2);
         std::vector<uint32_t> sorted = ids;
         std::sort(sorted.begin(), sorted.end(), [&](uint32_t a, uint32_t b) {
             return im.pat_len[a] != im.pat_len[b] ? im.pat_len[a] < im.pat_len[b] : a < b;
         });
-        im.bk_ids.insert(im.bk_ids.end(), sorted.begin(), sorted.end());
-        im.bk_start.push_back(uint32_t(im.bk_ids.size()));
+        im.bk_span.push_back(uint32_t(im.bk_entry.size() / 4));
+        im.bk_span.push_back(uint32_t(sorted.size()));
+        for (uint32_t id : sorted) {
+            im.bk_entry.push_back(id);
+            im.bk_entry.push_back(im.pat_len[id]);
+            im.bk_entry.push_back(uint32_t(im.pat_off[id]));
+            im.bk_entry.push_back(uint32_t(im.pat_off[id] >> 32));
+        }
     }
-    if (im.bk_ids.empty()) im.bk_ids.push_back(0);
+    if (im.bk_span.empty()) im.bk_span.assign(2, 0);
+    if (im.bk_entry.empty()) im.bk_entry.assign(4, 0);
 
     // ---- node records ------------------------------------------------------
     const uint32_t sigma = t.alphabet.size();
@@ -287,15 +293,21 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             const uint32_t bits =
                 std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, opt.max_filter_bits);
             im.filter_bits = bits;
-            im.filter_hashes = 1;
             im.filter.assign((size_t(1) << bits) / 32, 0u);
+            const uint32_t bits2 =
+                std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter2_slack, 16, opt.max_filter2_bits);
+            im.filter2_bits = bits2;
+            im.filter2.assign((size_t(1) << bits2) / 32, 0u);
             for (uint64_t g : grams) {
                 const uint32_t k32 = filter_fold(g);
                 im.filter[filter_word(k32, bits - 5)] |= filter_mask_bit(k32);
+                const uint32_t s2 = filter2_slot(k32, bits2);
+                im.filter2[s2 >> 5] |= 1u << (s2 & 31);
             }
         }
     }
     if (im.filter.empty()) im.filter.push_back(0);
+    if (im.filter2.empty()) im.filter2.push_back(0);
 
     for (uint32_t u = 0; u < n; ++u)
         if (t.terminal(u) && u != 0) (im.term_id[u] == kNoId ? im.keyed_terminals : im.private_terminals)++;

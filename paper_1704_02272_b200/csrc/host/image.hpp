@@ -26,11 +26,11 @@ struct GpuImage {
     std::vector<uint32_t> ht_id;
     uint64_t ht_mask = 0, hmul = 0;
 
-    std::vector<uint32_t> bk_start, bk_ids;
+    std::vector<uint32_t> bk_span, bk_entry; // uint2 / uint4 records, see layout.hpp
 
-    uint32_t filter_k = 0, filter_bits = 0, filter_hashes = 1;
+    uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
     uint64_t filter_paths = 0;
-    std::vector<uint32_t> filter;
+    std::vector<uint32_t> filter, filter2;
 
     uint32_t min_emit = UINT32_MAX; // shortest depth at which any start can report
     uint64_t reach = 0;             // max bytes one start may read; UINT64_MAX = unbounded
@@ -42,7 +42,8 @@ struct GpuImage {
 struct ImageOptions {
     uint32_t max_filter_bits = 20; // bitmap of 2^bits bits kept in shared memory (128 KiB)
     uint32_t filter_slack = 6;     // bits above log2(#k-grams): density <= 2^-slack
-    uint32_t filter_hashes = 1;    // Bloom probes per start
+    uint32_t filter2_slack = 10;   // second level: bits above log2(#k-grams)
+    uint32_t max_filter2_bits = 27; // 16 MiB in global memory
 };
 
 ImageOptions image_options_from_env();
