@@ -170,20 +170,24 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 
 // One failure-less walk (scan.cpp:20-51).  Each step issues a single record
 // load that yields both the current node's flags (terminal / bucket) and the
-// transition for the next byte.  `s_txt` / `s_room`: the start's bytes that
-// are staged in shared memory (the rest come from global memory).
+// transition for the next byte.  Text bytes come from a register window of 8
+// (`win`, the caller's copy of text[start, start + 8)), refilled 8 bytes at a
+// time, so a step waits on one load, not two.
 template <bool GROUPED, bool IDENT>
-__device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, const uint8_t* s_txt,
-                                     uint32_t s_room, Sink& sink)
+__device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
+                                     Sink& sink)
 {
     const TrieView& t = a.trie;
-    const uint8_t* txt = a.text + start;
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
     const uint32_t limit = t.depth_limit ? t.depth_limit : 0xFFFFFFFFu;
-    uint32_t node = 0, depth = 0;
+    uint32_t node = 0, depth = 0, wpos = 0;
     for (;;) {
         const bool more = depth < room;
-        const uint32_t byte = more ? (depth < s_room ? uint32_t(s_txt[depth]) : uint32_t(__ldg(txt + depth))) : 0u;
+        if (wpos == 8) { // next 8 bytes (the padded buffer makes the overread safe)
+            win = (uint64_t(text_word(a, start + depth + 4)) << 32) | text_word(a, start + depth);
+            wpos = 0;
+        }
+        const uint32_t byte = more ? uint32_t(win >> (8 * wpos)) & 0xFFu : 0u;
         const uint32_t sym = IDENT ? byte : uint32_t(s_sym[byte]);
         const bool step = more && (IDENT || sym != kNoSym);
         uint32_t word, base, meta, inline_id = kNoId;
@@ -216,6 +220,7 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
         if (!((word >> b) & 1u)) break;
         node = base + uint32_t(__popc(word & ((1u << b) - 1u)));
         ++depth;
+        ++wpos;
     }
 }
 
@@ -289,18 +294,16 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
 
 // ---- the walk stage of one warp ---------------------------------------------------
 
-// Second-level filter probe of the start at global offset `start` (text read
-// back from L2, where the TMA copy just streamed it).
+// Second-level filter: the start's key from its first text bytes `win`.
 template <int KW>
-__device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
+__device__ __forceinline__ bool probe2(const TrieView& t, uint64_t win)
 {
-    const TrieView& t = a.trie;
     const uint32_t k = t.filter_k;
-    uint32_t key = text_word(a, start);
+    uint32_t key = uint32_t(win);
     if (KW == 1) key &= (1u << (8 * k)) - 1u;
     if (KW == 2) {
         const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u);
-        key ^= (text_word(a, start + 4) & mhi) * 0x85EBCA77u; // filter_fold
+        key ^= (uint32_t(win >> 32) & mhi) * 0x85EBCA77u; // filter_fold
     }
     const uint32_t slot = filter2_slot(key, t.filter2_bits);
     return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
@@ -315,53 +318,51 @@ struct Walker {
     hepfac_match_t* region;
     uint64_t cursor; // records this warp has staged so far
 
-    // Candidates [0, n) of the tile starting at `lo`: second-level probe,
-    // then walk the survivors and append their records in start order.
+    // Candidates [0, n) of the tile starting at `lo`, 128 at a time (4 per
+    // lane, all loads in flight together): read each start's first 8 bytes
+    // back from L2, second-level probe, walk the survivors, append their
+    // records in start order.
     __device__ __forceinline__ void flush(uint64_t lo, uint32_t n)
     {
-        uint32_t ns = n;
-        if (KW != 0 && a.trie.filter2_bits) {
-            ns = 0;
-            const uint32_t below = (1u << lane) - 1u;
-            for (uint32_t r0 = 0; r0 < n; r0 += 32) {
-                const uint32_t e = r0 + lane;
-                uint16_t off = 0;
-                bool keep = false;
-                if (e < n) {
-                    off = q[e];
-                    keep = probe2<KW>(a, lo + off);
+        constexpr int kPer = 2;
+        const bool second = KW != 0 && a.trie.filter2_bits;
+        for (uint32_t r0 = 0; r0 < n; r0 += 32 * kPer) {
+            uint64_t start[kPer], win[kPer];
+            bool keep[kPer];
+#pragma unroll
+            for (int s = 0; s < kPer; ++s) {
+                const uint32_t e = r0 + 32 * s + lane;
+                keep[s] = e < n;
+                start[s] = lo + (keep[s] ? q[e] : 0u);
+                win[s] = keep[s] ? (uint64_t(text_word(a, start[s] + 4)) << 32) | text_word(a, start[s]) : 0ull;
+            }
+            if (second) {
+#pragma unroll
+                for (int s = 0; s < kPer; ++s) keep[s] = keep[s] && probe2<KW>(a.trie, win[s]);
+            }
+#pragma unroll
+            for (int s = 0; s < kPer; ++s) {
+                if (!__any_sync(0xFFFFFFFFu, keep[s])) continue;
+                Sink sink;
+                if (keep[s]) walk<GROUPED, IDENT>(a, s_sym, start[s], win[s], sink);
+                uint32_t tot;
+                const uint32_t ex = warp_exclusive(sink.n, lane, tot);
+                if (sink.n) {
+                    const uint64_t at = cursor + ex;
+                    uint4* dst = reinterpret_cast<uint4*>(region);
+                    if (at < a.warp_cap) dst[at] = sink.r0;
+                    if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
+                    if (sink.n > kRegRecords) { // rare: re-walk and write the rest directly
+                        Sink wr;
+                        wr.dst = region;
+                        wr.at = at + kRegRecords;
+                        wr.cap = a.warp_cap;
+                        wr.skip = kRegRecords;
+                        walk<GROUPED, IDENT>(a, s_sym, start[s], win[s], wr);
+                    }
                 }
-                const uint32_t b = __ballot_sync(0xFFFFFFFFu, keep); // every read of this round is done
-                if (keep) q[ns + __popc(b & below)] = off;          // compaction in place, order kept
-                ns += __popc(b);
+                cursor += tot;
             }
-            __syncwarp();
-        }
-        for (uint32_t r0 = 0; r0 < ns; r0 += 32) {
-            const uint32_t e = r0 + lane;
-            Sink sink;
-            uint64_t start = 0;
-            if (e < ns) {
-                start = lo + q[e];
-                walk<GROUPED, IDENT>(a, s_sym, start, nullptr, 0, sink);
-            }
-            uint32_t tot;
-            const uint32_t ex = warp_exclusive(sink.n, lane, tot);
-            if (sink.n) {
-                const uint64_t at = cursor + ex;
-                uint4* dst = reinterpret_cast<uint4*>(region);
-                if (at < a.warp_cap) dst[at] = sink.r0;
-                if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
-                if (sink.n > kRegRecords) { // rare: re-walk and write the rest directly
-                    Sink wr;
-                    wr.dst = region;
-                    wr.at = at + kRegRecords;
-                    wr.cap = a.warp_cap;
-                    wr.skip = kRegRecords;
-                    walk<GROUPED, IDENT>(a, s_sym, start, nullptr, 0, wr);
-                }
-            }
-            cursor += tot;
         }
         __syncwarp();
     }
