@@ -294,16 +294,18 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
 
 // ---- the walk stage of one warp ---------------------------------------------------
 
-// Second-level filter: the start's key from its first text bytes `win`.
+// Second-level filter probe of the start at global offset `start` (text read
+// back from L2, where the TMA copy just streamed it).
 template <int KW>
-__device__ __forceinline__ bool probe2(const TrieView& t, uint64_t win)
+__device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
 {
+    const TrieView& t = a.trie;
     const uint32_t k = t.filter_k;
-    uint32_t key = uint32_t(win);
+    uint32_t key = text_word(a, start);
     if (KW == 1) key &= (1u << (8 * k)) - 1u;
     if (KW == 2) {
         const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u);
-        key ^= (uint32_t(win >> 32) & mhi) * 0x85EBCA77u; // filter_fold
+        key ^= (text_word(a, start + 4) & mhi) * 0x85EBCA77u; // filter_fold
     }
     const uint32_t slot = filter2_slot(key, t.filter2_bits);
     return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
@@ -318,51 +320,55 @@ struct Walker {
     hepfac_match_t* region;
     uint64_t cursor; // records this warp has staged so far
 
-    // Candidates [0, n) of the tile starting at `lo`, 128 at a time (4 per
-    // lane, all loads in flight together): read each start's first 8 bytes
-    // back from L2, second-level probe, walk the survivors, append their
-    // records in start order.
+    // Candidates [0, n) of the tile starting at `lo`: second-level probe,
+    // then walk the survivors and append their records in start order.
     __device__ __forceinline__ void flush(uint64_t lo, uint32_t n)
     {
-        constexpr int kPer = 2;
-        const bool second = KW != 0 && a.trie.filter2_bits;
-        for (uint32_t r0 = 0; r0 < n; r0 += 32 * kPer) {
-            uint64_t start[kPer], win[kPer];
-            bool keep[kPer];
-#pragma unroll
-            for (int s = 0; s < kPer; ++s) {
-                const uint32_t e = r0 + 32 * s + lane;
-                keep[s] = e < n;
-                start[s] = lo + (keep[s] ? q[e] : 0u);
-                win[s] = keep[s] ? (uint64_t(text_word(a, start[s] + 4)) << 32) | text_word(a, start[s]) : 0ull;
-            }
-            if (second) {
-#pragma unroll
-                for (int s = 0; s < kPer; ++s) keep[s] = keep[s] && probe2<KW>(a.trie, win[s]);
-            }
-#pragma unroll
-            for (int s = 0; s < kPer; ++s) {
-                if (!__any_sync(0xFFFFFFFFu, keep[s])) continue;
-                Sink sink;
-                if (keep[s]) walk<GROUPED, IDENT>(a, s_sym, start[s], win[s], sink);
-                uint32_t tot;
-                const uint32_t ex = warp_exclusive(sink.n, lane, tot);
-                if (sink.n) {
-                    const uint64_t at = cursor + ex;
-                    uint4* dst = reinterpret_cast<uint4*>(region);
-                    if (at < a.warp_cap) dst[at] = sink.r0;
-                    if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
-                    if (sink.n > kRegRecords) { // rare: re-walk and write the rest directly
-                        Sink wr;
-                        wr.dst = region;
-                        wr.at = at + kRegRecords;
-                        wr.cap = a.warp_cap;
-                        wr.skip = kRegRecords;
-                        walk<GROUPED, IDENT>(a, s_sym, start[s], win[s], wr);
-                    }
+        uint32_t ns = n;
+        if (KW != 0 && a.trie.filter2_bits) {
+            ns = 0;
+            const uint32_t below = (1u << lane) - 1u;
+            for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+                const uint32_t e = r0 + lane;
+                uint16_t off = 0;
+                bool keep = false;
+                if (e < n) {
+                    off = q[e];
+                    keep = probe2<KW>(a, lo + off);
                 }
-                cursor += tot;
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, keep); // every read of this round is done
+                if (keep) q[ns + __popc(b & below)] = off;          // compaction in place, order kept
+                ns += __popc(b);
             }
+            __syncwarp();
+        }
+        for (uint32_t r0 = 0; r0 < ns; r0 += 32) {
+            const uint32_t e = r0 + lane;
+            Sink sink;
+            uint64_t start = 0;
+            uint64_t win = 0;
+            if (e < ns) {
+                start = lo + q[e];
+                win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
+                walk<GROUPED, IDENT>(a, s_sym, start, win, sink);
+            }
+            uint32_t tot;
+            const uint32_t ex = warp_exclusive(sink.n, lane, tot);
+            if (sink.n) {
+                const uint64_t at = cursor + ex;
+                uint4* dst = reinterpret_cast<uint4*>(region);
+                if (at < a.warp_cap) dst[at] = sink.r0;
+                if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
+                if (sink.n > kRegRecords) { // rare: re-walk and write the rest directly
+                    Sink wr;
+                    wr.dst = region;
+                    wr.at = at + kRegRecords;
+                    wr.cap = a.warp_cap;
+                    wr.skip = kRegRecords;
+                    walk<GROUPED, IDENT>(a, s_sym, start, win, wr);
+                }
+            }
+            cursor += tot;
         }
         __syncwarp();
     }
