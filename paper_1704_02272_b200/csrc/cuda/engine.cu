@@ -189,6 +189,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_k = im.filter_k;
     v.filter2 = d->upload(im.filter2);
     v.filter2_bits = im.filter2_bits;
+    v.jump = d->upload(im.jump);
+    v.jump_bits = im.jump_bits;
     v.min_emit = im.min_emit;
 
     d->kernel = select_kernel(d->grouped, d->identity, d->kw);

@@ -60,16 +60,24 @@ HFB_HD uint32_t filter_mask_bit(uint32_t key32) { return 0x80000000u >> (key32 &
 
 // Second-level filter (global memory, L2-resident): an independent mixing hash
 // of the same folded key into a larger bitmap.  Only first-level survivors
-// (about 2%) probe it.
-HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits)
+// (about 2%) probe it.  The top bits of the same mix index the jump table.
+HFB_HD uint32_t filter2_hash(uint32_t x)
 {
     x ^= x >> 16;
     x *= 0x7FEB352Du;
     x ^= x >> 15;
     x *= 0x846CA68Bu;
     x ^= x >> 16;
-    return x >> (32 - bits);
+    return x;
 }
+HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x) >> (32 - bits); }
+
+// Jump table: every depth-k path string (k = filter_k bytes, little-endian in
+// {lo, hi}) -> the node it reaches.  No node above depth k can report
+// (k <= min_emit), so a walk may start there instead of at the root.  Open
+// addressing, load <= 1/2, 16-byte slots {lo, hi, node, 0}; node == kNoId
+// marks an empty slot.
+HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {
@@ -94,6 +102,8 @@ struct TrieView {
     uint32_t filter_k;
     const uint32_t* filter2; // second level, 2^filter2_bits bits
     uint32_t filter2_bits;   // 0 = no second level
+    const uint32_t* jump;    // 2^jump_bits uint4 slots
+    uint32_t jump_bits;      // 0 = no jump table (walks start at the root)
     uint32_t min_emit;
 };
 

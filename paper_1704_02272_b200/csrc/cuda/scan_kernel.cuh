@@ -40,7 +40,7 @@ namespace hfb::gpu {
 namespace cg = cooperative_groups;
 
 #ifndef HFB_WARPS
-#define HFB_WARPS 20
+#define HFB_WARPS 16
 #endif
 #ifndef HFB_STAGES
 #define HFB_STAGES 2
@@ -173,14 +173,17 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 // transition for the next byte.  Text bytes come from a register window of 8
 // (`win`, the caller's copy of text[start, start + 8)), refilled 8 bytes at a
 // time, so a step waits on one load, not two.
+//
+// A walk may begin below the root: (node, depth) from the jump table, which
+// is only used for depth <= min_emit, where nothing above can report.
 template <bool GROUPED, bool IDENT>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
-                                     Sink& sink)
+                                     uint32_t node, uint32_t depth, Sink& sink)
 {
     const TrieView& t = a.trie;
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
     const uint32_t limit = t.depth_limit ? t.depth_limit : 0xFFFFFFFFu;
-    uint32_t node = 0, depth = 0, wpos = 0;
+    uint32_t wpos = depth; // depth <= 8 here
     for (;;) {
         const bool more = depth < room;
         if (wpos == 8) { // next 8 bytes (the padded buffer makes the overread safe)
@@ -311,6 +314,23 @@ __device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
     return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
 }
 
+// The node a start reaches after its first k bytes (`win` = text[start,
+// start + 8)), or kNoId when no trie path spells them.
+template <int KW>
+__device__ __forceinline__ uint32_t jump_node(const TrieView& t, uint64_t win)
+{
+    const uint32_t k = t.filter_k;
+    uint32_t lo = uint32_t(win), hi = 0;
+    if (KW == 1) lo &= (1u << (8 * k)) - 1u;
+    if (KW == 2) hi = uint32_t(win >> 32) & (k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u));
+    const uint32_t mask = (1u << t.jump_bits) - 1u;
+    const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
+    for (uint32_t s = jump_slot(lo ^ (hi * 0x85EBCA77u), t.jump_bits);; s = (s + 1) & mask) {
+        const uint4 e = __ldg(slots + s);
+        if (e.z == kNoId || (e.x == lo && e.y == hi)) return e.z;
+    }
+}
+
 template <bool GROUPED, bool IDENT, int KW>
 struct Walker {
     const ScanArgs& a;
@@ -347,10 +367,15 @@ struct Walker {
             Sink sink;
             uint64_t start = 0;
             uint64_t win = 0;
+            uint32_t node = 0, depth = 0;
             if (e < ns) {
                 start = lo + q[e];
                 win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
-                walk<GROUPED, IDENT>(a, s_sym, start, win, sink);
+                if (KW != 0 && a.trie.jump_bits) {
+                    node = jump_node<KW>(a.trie, win);
+                    depth = a.trie.filter_k;
+                }
+                if (node != kNoId) walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, sink);
             }
             uint32_t tot;
             const uint32_t ex = warp_exclusive(sink.n, lane, tot);
@@ -365,7 +390,7 @@ struct Walker {
                     wr.at = at + kRegRecords;
                     wr.cap = a.warp_cap;
                     wr.skip = kRegRecords;
-                    walk<GROUPED, IDENT>(a, s_sym, start, win, wr);
+                    walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, wr);
                 }
             }
             cursor += tot;

@@ -26,7 +26,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + jump.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -40,6 +40,7 @@ ImageOptions image_options_from_env()
         long v = std::strtol(s, nullptr, 10);
         if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
     }
+    if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER2_SLACK")) {
         long v = std::strtol(s, nullptr, 10);
         if (v >= 0 && v <= 16) o.filter2_slack = uint32_t(v);
@@ -262,6 +263,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         const uint32_t k = std::min(im.min_emit, kMaxFilterKey);
         im.filter_k = k;
         std::vector<uint64_t> grams;
+        std::vector<uint32_t> gram_node;
         const uint64_t cap = uint64_t(1) << 22;
         struct Frame {
             uint32_t node, depth;
@@ -274,6 +276,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             st.pop_back();
             if (f.depth == k) {
                 grams.push_back(f.key);
+                gram_node.push_back(f.node);
                 overflow = grams.size() > cap;
                 continue;
             }
@@ -304,10 +307,25 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 const uint32_t s2 = filter2_slot(k32, bits2);
                 im.filter2[s2 >> 5] |= 1u << (s2 & 31);
             }
+            if (opt.jump) {
+                const uint32_t jb = std::max<uint32_t>(ceil_log2(grams.size()) + 1, 4);
+                const uint32_t mask = (1u << jb) - 1u;
+                im.jump_bits = jb;
+                im.jump.assign(size_t(4) << jb, 0u);
+                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[4 * s + 2] = kNoId;
+                for (size_t i = 0; i < grams.size(); ++i) {
+                    uint32_t s = jump_slot(filter_fold(grams[i]), jb);
+                    while (im.jump[4 * s + 2] != kNoId) s = (s + 1) & mask;
+                    im.jump[4 * s + 0] = uint32_t(grams[i]);
+                    im.jump[4 * s + 1] = uint32_t(grams[i] >> 32);
+                    im.jump[4 * s + 2] = gram_node[i];
+                }
+            }
         }
     }
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
+    if (im.jump.empty()) im.jump.assign(4, 0u);
 
     for (uint32_t u = 0; u < n; ++u)
         if (t.terminal(u) && u != 0) (im.term_id[u] == kNoId ? im.keyed_terminals : im.private_terminals)++;

@@ -31,6 +31,8 @@ struct GpuImage {
     uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
     uint64_t filter_paths = 0;
     std::vector<uint32_t> filter, filter2;
+    uint32_t jump_bits = 0;     // log2 slots of the depth-k jump table, 0 = none
+    std::vector<uint32_t> jump; // uint4 slots, see layout.hpp
 
     uint32_t min_emit = UINT32_MAX; // shortest depth at which any start can report
     uint64_t reach = 0;             // max bytes one start may read; UINT64_MAX = unbounded
@@ -44,6 +46,7 @@ struct ImageOptions {
     uint32_t filter_slack = 6;     // bits above log2(#k-grams): density <= 2^-slack
     uint32_t filter2_slack = 10;   // second level: bits above log2(#k-grams)
     uint32_t max_filter2_bits = 27; // 16 MiB in global memory
+    bool jump = true;               // depth-k jump table (HEPFAC_JUMP=0 disables)
 };
 
 ImageOptions image_options_from_env();
