@@ -81,6 +81,8 @@ typedef struct hepfac_b200_layout_info {
     uint64_t device_bytes;
     uint64_t private_terminals;
     uint64_t keyed_terminals;
+    uint32_t filter_mode;     /* 0 none, 1 single probe per start, 2 pair probes (one per two starts) */
+    uint32_t filter_pass_ppm; /* estimated random starts per million that reach the walk queue */
 } hepfac_b200_layout_info_t;
 
 hepfac_status_t hepfac_b200_layout_info(const hepfac_trie_t* trie, hepfac_b200_layout_info_t* out);

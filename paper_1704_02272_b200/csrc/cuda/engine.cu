@@ -111,6 +111,8 @@ struct DeviceTrie {
     TrieView view{};
     bool grouped = false, identity = false;
     int kw = 0;
+    bool pair = false;
+    double filter_pass = 1.0;
     KernelFn kernel = nullptr;
     size_t smem = 0;
     int blocks_per_sm = 1, sm_count = 1;
@@ -138,15 +140,20 @@ struct DeviceTrie {
 
 namespace {
 
-KernelFn select_kernel(bool grouped, bool identity, int kw)
+KernelFn select_kernel(bool grouped, bool identity, int kw, bool pair)
 {
     using namespace gpu;
-    // identity byte maps only exist at sigma = 256, i.e. the grouped layout
-#define HFB_KW(G, I) {pfac_scan_kernel<G, I, 0>, pfac_scan_kernel<G, I, 1>, pfac_scan_kernel<G, I, 2>, pfac_scan_kernel<G, I, 3>}
-    static const KernelFn table[2][2][4] = {{HFB_KW(false, false), HFB_KW(false, false)},
-                                            {HFB_KW(true, false), HFB_KW(true, true)}};
+    // identity byte maps only exist at sigma = 256, i.e. the grouped layout;
+    // the pair filter needs k >= 4 (kw 2 or 3)
+#define HFB_KW(G, I)                                                                                       \
+    {{pfac_scan_kernel<G, I, 0, false>, pfac_scan_kernel<G, I, 0, false>},                                 \
+     {pfac_scan_kernel<G, I, 1, false>, pfac_scan_kernel<G, I, 1, false>},                                 \
+     {pfac_scan_kernel<G, I, 2, false>, pfac_scan_kernel<G, I, 2, true>},                                  \
+     {pfac_scan_kernel<G, I, 3, false>, pfac_scan_kernel<G, I, 3, true>}}
+    static const KernelFn table[2][2][4][2] = {{HFB_KW(false, false), HFB_KW(false, false)},
+                                               {HFB_KW(true, false), HFB_KW(true, true)}};
 #undef HFB_KW
-    return table[grouped][identity && grouped][kw];
+    return table[grouped][identity && grouped][kw][pair ? 1 : 0];
 }
 
 std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
@@ -163,6 +170,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     d->node_count = im.node_count;
     d->groups = im.groups;
     d->filter_paths = im.filter_paths;
+    d->filter_pass = im.filter_pass;
     d->device_bytes = im.device_bytes();
     d->private_terminals = im.private_terminals;
     d->keyed_terminals = im.keyed_terminals;
@@ -187,13 +195,15 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_words = d->kw ? uint32_t(im.filter.size()) : 0u;
     v.filter_bits = im.filter_bits;
     v.filter_k = im.filter_k;
+    v.pair_shift = im.pair_shift;
     v.filter2 = d->upload(im.filter2);
     v.filter2_bits = im.filter2_bits;
     v.jump = d->upload(im.jump);
     v.jump_bits = im.jump_bits;
     v.min_emit = im.min_emit;
 
-    d->kernel = select_kernel(d->grouped, d->identity, d->kw);
+    d->pair = im.filter_mode == 2;
+    d->kernel = select_kernel(d->grouped, d->identity, d->kw, d->pair);
     d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes();
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
@@ -601,6 +611,8 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
+    li.filter_mode = d->kw == 0 ? 0u : (d->pair ? 2u : 1u);
+    li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }
 

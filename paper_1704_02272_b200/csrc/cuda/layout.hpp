@@ -46,17 +46,35 @@ HFB_HD uint64_t mix64(uint64_t k)
     return k;
 }
 
-// Start filter: the first k text bytes (little-endian packed into a 64-bit
-// key) are folded to 32 bits; the bitmap word comes from a multiplicative
-// hash of the folded key, the bit inside the word from its low 5 bits (the
-// first byte).  Bits are stored MSB-first, so the kernel brings a bit to the
-// top with one wrapping funnel shift by the key itself.
+// Start filter, single-probe form: the first k text bytes (little-endian
+// packed into a 64-bit key) are folded to 32 bits; the bitmap word comes from
+// the high half of a 32x32-bit product (IMAD.HI, then one AND with the word
+// mask scaled to bytes), the bit inside the word from the key's low 5 bits
+// (the first byte).  Bits are stored MSB-first, so the kernel brings a bit to
+// the top with one wrapping funnel shift by the key itself.
+constexpr uint32_t kFilterMul = 0x9E3779B1u;
 HFB_HD uint32_t filter_fold(uint64_t key)
 {
     return uint32_t(key) ^ (uint32_t(key >> 32) * 0x85EBCA77u);
 }
-HFB_HD uint32_t filter_word(uint32_t key32, uint32_t word_bits) { return (key32 * 0x9E3779B1u) >> (32 - word_bits); }
+HFB_HD uint32_t filter_word(uint32_t key32, uint32_t word_bits)
+{
+    return uint32_t((uint64_t(key32) * kFilterMul) >> 34) & ((1u << word_bits) - 1u);
+}
 HFB_HD uint32_t filter_mask_bit(uint32_t key32) { return 0x80000000u >> (key32 & 31u); }
+
+// Start filter, pair form (k >= 4).  One 32-bit word per 3-byte "middle"
+// M = (b1, b2, b3) serves two starts: the start at M's first byte (its 4th
+// byte selects the bit: role B) and the start one byte earlier (its 1st byte
+// selects the bit: role A), superimposed in the same word.  Text position i
+// (odd, inside a 32-start lane slice) probes the middle at i and tests start
+// i-1 as role A and start i as role B, so 32 starts cost 16 probes; the other
+// role of each survivor is tested afterwards (second level, same table).
+// A depth-k path p0 p1 p2 p3 ... sets bit p0 of word H(p1 p2 p3) and bit p3 of
+// word H(p0 p1 p2).  H is multiply-shift over the low 24 bits of the packed
+// middle (the multiplier's low byte is zero, so the 4th byte drops out).
+constexpr uint32_t kPairMul = 0x2545F491u << 8;
+HFB_HD uint32_t pair_word(uint32_t middle, uint32_t word_bits) { return (middle * kPairMul) >> (32 - word_bits); }
 
 // Second-level filter (global memory, L2-resident): an independent mixing hash
 // of the same folded key into a larger bitmap.  Only first-level survivors
@@ -100,6 +118,7 @@ struct TrieView {
     uint32_t filter_words;
     uint32_t filter_bits; // 0 = filter disabled (every start walks)
     uint32_t filter_k;
+    uint32_t pair_shift;  // pair form: 32 - log2(words), i.e. word = (middle * kPairMul) >> pair_shift
     const uint32_t* filter2; // second level, 2^filter2_bits bits
     uint32_t filter2_bits;   // 0 = no second level
     const uint32_t* jump;    // 2^jump_bits uint4 slots

@@ -237,7 +237,7 @@ __device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_
 {
     if (KW == 0) return valid;
     const uint32_t k = t.filter_k;
-    const uint32_t shift = 30u - (t.filter_bits - 5u); // hash -> byte offset of the bitmap word
+    const uint32_t mask4 = (t.filter_words - 1u) << 2; // hash -> byte offset of the bitmap word
     const uint32_t m32 = (KW == 3 || k >= 4) ? 0xFFFFFFFFu : ((1u << (8 * k)) - 1u);
     const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
     const uint8_t* fbytes = reinterpret_cast<const uint8_t*>(s_filter);
@@ -253,11 +253,63 @@ __device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_
         } else {
             key = KW == 3 ? lo : (lo & m32);
         }
-        const uint32_t off = ((key * 0x9E3779B1u) >> shift) & ~3u; // filter_word(key) * 4
+        const uint32_t off = __umulhi(key, kFilterMul) & mask4; // filter_word(key) * 4
         const uint32_t word = *reinterpret_cast<const uint32_t*>(fbytes + off);
         m = __funnelshift_l(__funnelshift_l(0u, word, key), m, 1); // (m << 1) | bit (key & 31), MSB-first
     }
     return __brev(m) & valid; // start j at bit j
+}
+
+// 32-bit word at byte offset `off` of dynamic shared memory (the start
+// filter table lives at offset 0).  Addressing the symbol directly lets ptxas
+// fold its window offset into the LDS immediate.
+__device__ __forceinline__ uint32_t table_word(uint32_t off)
+{
+    uint32_t v;
+    asm("{\n\t.reg .u32 b;\n\tmov.u32 b, _ZN3hfb3gpu4smemE;\n\tadd.u32 b, b, %1;\n\tld.shared.u32 %0, [b];\n\t}"
+        : "=r"(v)
+        : "r"(off));
+    return v;
+}
+
+// Pair form (layout.hpp): 16 probes for the lane's 32 starts.  Probe p reads
+// the word of the middle at odd position i = 2p + 1 and tests start i - 1
+// (role A: bit of its first byte) and start i (role B: bit of its 4th byte).
+// Returns bit j = start j passed its first role.
+__device__ __forceinline__ uint32_t filter_pair(const uint32_t (&w)[10], uint32_t shift, uint32_t valid)
+{
+    uint32_t m = 0; // start j ends up at bit 31 - j
+#pragma unroll
+    for (int i = 1; i < int(kLaneStarts); i += 2) {
+        // window(n) = text bytes n..n+3 of the lane slice
+        const uint32_t mid = __funnelshift_r(w[i >> 2], w[(i >> 2) + 1], 8 * (i & 3));
+        const int a = i - 1, b = i + 3; // even positions
+        const uint32_t amt_a = (a & 3) ? __funnelshift_r(w[a >> 2], w[(a >> 2) + 1], 16) : w[a >> 2];
+        const uint32_t amt_b = (b & 3) ? __funnelshift_r(w[b >> 2], w[(b >> 2) + 1], 16) : w[b >> 2];
+        const uint32_t word = table_word(((mid * kPairMul) >> shift) << 2); // pair_word(mid) * 4
+        m = __funnelshift_l(__funnelshift_l(0u, word, amt_a), m, 1); // start i - 1
+        m = __funnelshift_l(__funnelshift_l(0u, word, amt_b), m, 1); // start i
+    }
+    return __brev(m) & valid;
+}
+
+// Second pair level: each survivor j of `mask` tests its other role (odd j:
+// role A at the middle j + 1; even j: role B at the middle j), reading its 4
+// bytes back from the staged lane slice `src` in shared memory.
+__device__ __forceinline__ uint32_t filter_pair_second(uint32_t mask, const uint8_t* src, uint32_t shift)
+{
+    uint32_t keep = 0;
+    for (uint32_t c = mask; c; c &= c - 1) {
+        const uint32_t j = __ffs(c) - 1;
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(src + (j & ~3u));
+        const uint32_t y = __funnelshift_r(wp[0], wp[1], 8 * (j & 3)); // bytes j..j+3
+        const bool odd = j & 1u;
+        const uint32_t mid = odd ? (y >> 8) : y;
+        const uint32_t amt = odd ? y : (y >> 24);
+        const uint32_t word = table_word(((mid * kPairMul) >> shift) << 2);
+        keep |= ((word << (amt & 31u)) >> 31) << j;
+    }
+    return keep;
 }
 
 // ---- warp helpers ---------------------------------------------------------------
@@ -437,7 +489,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 // Shared-memory bytes a CTA needs beyond the filter bitmap.
 constexpr uint32_t smem_fixed_bytes() { return kWarps * kStages * kStageBytes + kWarps * kQueue * 2 + 512; }
 
-template <bool GROUPED, bool IDENT, int KW>
+template <bool GROUPED, bool IDENT, int KW, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a)
 {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -504,7 +556,12 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
                 const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
                 const uint2 x = *reinterpret_cast<const uint2*>(src + 32);
                 const uint32_t w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, x.x, x.y};
-                mask = filter_mask<KW>(t, w, s_filter, valid);
+                if (PAIR) {
+                    mask = filter_pair(w, t.pair_shift, valid);
+                    mask = filter_pair_second(mask, src, t.pair_shift);
+                } else {
+                    mask = filter_mask<KW>(t, w, s_filter, valid);
+                }
             }
             __syncwarp();
             if (lane == 0) produce(); // the stage is consumed: refill it

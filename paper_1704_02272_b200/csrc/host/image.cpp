@@ -17,7 +17,9 @@
 #include "image.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <string>
 #include <unordered_set>
 
 namespace hfb {
@@ -41,6 +43,10 @@ ImageOptions image_options_from_env()
         if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
     }
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
+    if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
+        const std::string m = s;
+        o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : 0u);
+    }
     if (const char* s = std::getenv("HEPFAC_FILTER2_SLACK")) {
         long v = std::strtol(s, nullptr, 10);
         if (v >= 0 && v <= 16) o.filter2_slack = uint32_t(v);
@@ -293,19 +299,98 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         if (grams.empty()) {
             im.min_emit = UINT32_MAX; // no start can reach a reporting depth
         } else if (!overflow) {
+            auto popcount = [](const std::vector<uint32_t>& v) {
+                uint64_t c = 0;
+                for (uint32_t w : v) c += uint64_t(__builtin_popcount(w));
+                return c;
+            };
+            // single-probe table over the whole k-byte key
             const uint32_t bits =
                 std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, opt.max_filter_bits);
-            im.filter_bits = bits;
-            im.filter.assign((size_t(1) << bits) / 32, 0u);
-            const uint32_t bits2 =
-                std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter2_slack, 16, opt.max_filter2_bits);
-            im.filter2_bits = bits2;
-            im.filter2.assign((size_t(1) << bits2) / 32, 0u);
+            std::vector<uint32_t> single((size_t(1) << bits) / 32, 0u);
             for (uint64_t g : grams) {
                 const uint32_t k32 = filter_fold(g);
-                im.filter[filter_word(k32, bits - 5)] |= filter_mask_bit(k32);
-                const uint32_t s2 = filter2_slot(k32, bits2);
-                im.filter2[s2 >> 5] |= 1u << (s2 & 31);
+                single[filter_word(k32, bits - 5)] |= filter_mask_bit(k32);
+            }
+            double f_single = double(popcount(single)) / double(uint64_t(1) << bits);
+            // pair table over the first 4 bytes (k >= 4)
+            std::vector<uint32_t> pair;
+            uint32_t pair_wb = 0;
+            double f_pair = 1.0;
+            if (k >= 4) {
+                pair_wb = std::clamp<uint32_t>(ceil_log2(2 * grams.size()) + opt.filter_slack, 10, opt.max_filter_bits) - 5;
+                pair.assign(size_t(1) << pair_wb, 0u);
+                for (uint64_t g : grams) {
+                    const uint32_t p = uint32_t(g); // p0 | p1 << 8 | p2 << 16 | p3 << 24
+                    pair[pair_word(p >> 8, pair_wb)] |= filter_mask_bit(p & 0xFFu);        // role A
+                    pair[pair_word(p & 0xFFFFFFu, pair_wb)] |= filter_mask_bit(p >> 24);   // role B
+                }
+                f_pair = double(popcount(pair)) / double(uint64_t(32) << pair_wb);
+            }
+            // Pass rates on text drawn uniformly from the alphabet (Monte Carlo,
+            // fixed seed): what fraction of starts survive each level.
+            double p_single = f_single, p_first = f_pair, p_both = f_pair * f_pair;
+            {
+                const uint32_t sigma = t.alphabet.size();
+                const uint32_t N = 1u << 15;
+                uint64_t x = 0x9E3779B97F4A7C15ull;
+                uint32_t n_single = 0, n_first = 0, n_both = 0;
+                auto word_bit = [](const std::vector<uint32_t>& tab, uint32_t word, uint32_t byte) {
+                    return (tab[word] & filter_mask_bit(byte)) != 0;
+                };
+                for (uint32_t s = 0; s < N; ++s) {
+                    uint64_t key = 0;
+                    for (uint32_t b = 0; b < k; ++b) {
+                        x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+                        key |= uint64_t(t.alphabet.byte_of(uint32_t(x % sigma))) << (8 * b);
+                    }
+                    const uint32_t k32 = filter_fold(key);
+                    n_single += word_bit(single, filter_word(k32, bits - 5), k32);
+                    if (k >= 4) {
+                        const uint32_t p = uint32_t(key);
+                        const bool a = word_bit(pair, pair_word(p >> 8, pair_wb), p & 0xFFu);
+                        const bool b = word_bit(pair, pair_word(p & 0xFFFFFFu, pair_wb), p >> 24);
+                        n_first += (s & 1) ? a : b; // odd starts meet role A first
+                        n_both += a && b;
+                    }
+                }
+                p_single = double(n_single) / N;
+                if (k >= 4) p_first = double(n_first) / N, p_both = double(n_both) / N;
+            }
+            // Cost per start in issue slots (shared-memory wavefronts counted
+            // like instructions): single = 6.75 SASS + 3.7 wavefronts; pair =
+            // 4.75 + 1.85, plus a divergent second probe per first-level
+            // survivor; each start reaching the walk queue costs ~60.
+            const double cost_single = 10.45 + 60.0 * p_single;
+            const double cost_pair = 6.6 + 30.0 * p_first + 60.0 * p_both;
+            bool use_pair = k >= 4 && cost_pair < cost_single;
+            f_single = p_single;
+            f_pair = std::sqrt(p_both);
+            if (opt.filter_mode == 1) use_pair = false;
+            if (opt.filter_mode == 2) use_pair = k >= 4;
+            if (use_pair) {
+                im.filter_mode = 2;
+                im.filter = std::move(pair);
+                im.filter_bits = pair_wb + 5;
+                im.pair_shift = 32 - pair_wb;
+                im.filter_pass = p_both;
+            } else {
+                im.filter_mode = 1;
+                im.filter = std::move(single);
+                im.filter_bits = bits;
+                im.filter_pass = p_single;
+            }
+            // Third level (L2-resident, whole k-byte key) when what reaches the
+            // walk queue is still dense.
+            if (im.filter_mode == 1 || im.filter_pass > 0.002) {
+                const uint32_t bits2 =
+                    std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter2_slack, 16, opt.max_filter2_bits);
+                im.filter2_bits = bits2;
+                im.filter2.assign((size_t(1) << bits2) / 32, 0u);
+                for (uint64_t g : grams) {
+                    const uint32_t s2 = filter2_slot(filter_fold(g), bits2);
+                    im.filter2[s2 >> 5] |= 1u << (s2 & 31);
+                }
             }
             if (opt.jump) {
                 const uint32_t jb = std::max<uint32_t>(ceil_log2(grams.size()) + 1, 4);

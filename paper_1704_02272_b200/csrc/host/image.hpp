@@ -29,6 +29,9 @@ struct GpuImage {
     std::vector<uint32_t> bk_span, bk_entry; // uint2 / uint4 records, see layout.hpp
 
     uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
+    uint32_t filter_mode = 0; // 0 none, 1 single probe, 2 pair probes (layout.hpp)
+    uint32_t pair_shift = 0;
+    double filter_pass = 1.0; // estimated fraction of random starts reaching the walk queue
     uint64_t filter_paths = 0;
     std::vector<uint32_t> filter, filter2;
     uint32_t jump_bits = 0;     // log2 slots of the depth-k jump table, 0 = none
@@ -47,6 +50,7 @@ struct ImageOptions {
     uint32_t filter2_slack = 10;   // second level: bits above log2(#k-grams)
     uint32_t max_filter2_bits = 27; // 16 MiB in global memory
     bool jump = true;               // depth-k jump table (HEPFAC_JUMP=0 disables)
+    uint32_t filter_mode = 0;       // 0 = cost model, 1 = single, 2 = pair (HEPFAC_FILTER_MODE)
 };
 
 ImageOptions image_options_from_env();

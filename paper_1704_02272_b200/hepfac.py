@@ -90,7 +90,8 @@ class _LayoutInfo(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in ("node_count", "groups", "record_bytes", "filter_k", "filter_bits",
                                           "min_emit", "smem_bytes", "blocks_per_sm", "sm_count", "identity")] + \
                [(n, C.c_uint64) for n in ("filter_paths", "reach", "device_bytes", "private_terminals",
-                                          "keyed_terminals")]
+                                          "keyed_terminals")] + \
+               [(n, C.c_uint32) for n in ("filter_mode", "filter_pass_ppm")]
 
 
 _P = C.c_void_p

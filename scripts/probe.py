@@ -54,7 +54,7 @@ def main():
                    "depth_limit": trie.depth_limit(), "gen_s": round(gen_s, 1), "build_s": round(build_s, 2),
                    "layout": {k: info[k] for k in ("record_bytes", "filter_k", "filter_bits", "filter_paths",
                                                    "min_emit", "smem_bytes", "blocks_per_sm", "reach",
-                                                   "keyed_terminals", "private_terminals")}}
+                                                   "keyed_terminals", "private_terminals", "filter_mode", "filter_pass_ppm")}}
             if args.check:
                 import oracle
                 ref = oracle.ref_library()
