@@ -14,6 +14,7 @@
 
 #include "../host/image.hpp"
 #include "engine.hpp"
+#include "filter_kernel.cuh"
 #include "scan_kernel.cuh"
 
 namespace hfb {
@@ -115,7 +116,11 @@ struct DeviceTrie {
     double filter_pass = 1.0;
     KernelFn kernel = nullptr;
     size_t smem = 0;
+    // pair pipeline: filter pass, then the candidate-walking pass (`kernel`)
+    size_t filter_smem = 0;
+    int filter_blocks_per_sm = 0;
     int blocks_per_sm = 1, sm_count = 1;
+    uint32_t warps = gpu::kWarps; // per CTA of `kernel`
     uint32_t min_emit = UINT32_MAX, node_count = 0, groups = 0;
     uint64_t reach = 0, filter_paths = 0, device_bytes = 0, private_terminals = 0, keyed_terminals = 0;
 
@@ -140,6 +145,13 @@ struct DeviceTrie {
 
 namespace {
 
+// HEPFAC_PAIR_PIPELINE=0 keeps pair-filter tries on the fused kernel.
+bool pair_pipeline_enabled()
+{
+    const char* s = std::getenv("HEPFAC_PAIR_PIPELINE");
+    return !s || std::strtol(s, nullptr, 10) != 0;
+}
+
 KernelFn select_kernel(bool grouped, bool identity, int kw, bool pair)
 {
     using namespace gpu;
@@ -154,6 +166,17 @@ KernelFn select_kernel(bool grouped, bool identity, int kw, bool pair)
                                                {HFB_KW(true, false), HFB_KW(true, true)}};
 #undef HFB_KW
     return table[grouped][identity && grouped][kw][pair ? 1 : 0];
+}
+
+// Second pass of the pair pipeline (kw 2 or 3).
+KernelFn select_cands_kernel(bool grouped, bool identity, int kw)
+{
+    using namespace gpu;
+#define HFB_C(G, I) {pfac_scan_kernel<G, I, 2, false, true>, pfac_scan_kernel<G, I, 3, false, true>}
+    static const KernelFn table[2][2][2] = {{HFB_C(false, false), HFB_C(false, false)},
+                                            {HFB_C(true, false), HFB_C(true, true)}};
+#undef HFB_C
+    return table[grouped][identity && grouped][kw == 3 ? 1 : 0];
 }
 
 std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
@@ -196,17 +219,32 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_bits = im.filter_bits;
     v.filter_k = im.filter_k;
     v.pair_shift = im.pair_shift;
+    v.pair_mul = im.pair_shift ? 1u << (32 - im.pair_shift) : 0u;
+    v.mul_shr8 = 1u << 24;
+    v.mul_shr16 = 1u << 16;
     v.filter2 = d->upload(im.filter2);
     v.filter2_bits = im.filter2_bits;
     v.jump = d->upload(im.jump);
     v.jump_bits = im.jump_bits;
     v.min_emit = im.min_emit;
 
-    d->pair = im.filter_mode == 2;
-    d->kernel = select_kernel(d->grouped, d->identity, d->kw, d->pair);
-    d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes();
+    d->pair = im.filter_mode == 2 && pair_pipeline_enabled();
+    if (d->pair) {
+        d->kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
+        d->smem = gpu::smem_fixed_bytes(true); // no filter table in the walking pass
+        d->warps = gpu::kCWarps;
+        d->filter_smem = size_t(v.filter_words) * 4 + gpu::filter_smem_fixed_bytes();
+        CK(cudaFuncSetAttribute(gpu::pfac_pair_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(d->filter_smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, gpu::pfac_pair_filter_kernel,
+                                                         gpu::kFThreads, d->filter_smem));
+        if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
+    } else {
+        d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
+        d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
+    }
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, gpu::kThreads, d->smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     CK(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device));
     return d;
@@ -250,8 +288,14 @@ struct Workspace {
     uint64_t chunk_cap = 0;
     unsigned long long* d_bases = nullptr; // streamed: records before chunk c
     uint64_t bases_cap = 0;
+    uint16_t* d_cand = nullptr;            // pair pipeline: per filter warp candidate regions
+    uint64_t cand_alloc = 0, cand_cap = 0;
+    uint32_t* d_tile_ccount = nullptr;
+    uint32_t* d_tile_cslot = nullptr;
+    uint64_t ctile_cap = 0, ctile_cap2 = 0;
     // [0] max records a warp needed (0 = fits), [1] total of the last launch,
-    // [2] error word, [3] zero (base_in of a single launch), [4] its base_out
+    // [2] error word, [3] zero (base_in of a single launch), [4] its base_out,
+    // [5] max candidates a filter warp needed (0 = fits)
     unsigned long long* d_small = nullptr;
     unsigned long long* h_small = nullptr; // pinned mirror
     uint4* d_flush = nullptr;
@@ -277,7 +321,7 @@ struct Workspace {
         cudaStreamSynchronize(copy);
         for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
                         (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
-                        (void*)d_flush})
+                        (void*)d_flush, (void*)d_cand, (void*)d_tile_ccount, (void*)d_tile_cslot})
             cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
@@ -322,8 +366,19 @@ struct Workspace {
         regrow(d_tile_slot, tile_cap2, tiles);
         regrow(d_chunk, chunk_cap, grid);
     }
-    // Clears the per-scan accumulators (overflow need, error word).
-    void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 5 * sizeof(unsigned long long), stream)); }
+    // cand_cap only grows on overflow, like warp_cap
+    void ensure_cand(uint64_t warps, uint64_t per_warp)
+    {
+        cand_cap = std::max(cand_cap, per_warp);
+        regrow(d_cand, cand_alloc, warps * cand_cap);
+    }
+    void ensure_ctiles(uint64_t tiles)
+    {
+        regrow(d_tile_ccount, ctile_cap, tiles);
+        regrow(d_tile_cslot, ctile_cap2, tiles);
+    }
+    // Clears the per-scan accumulators (overflow needs, error word).
+    void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 6 * sizeof(unsigned long long), stream)); }
 };
 
 std::mutex g_pool_mu;
@@ -364,15 +419,20 @@ uint64_t initial_records(uint64_t bytes) { return std::max<uint64_t>(1u << 14, b
 
 struct Launch {
     uint64_t n_tiles = 0, grid = 0, warps = 0;
+    uint64_t n_ftiles = 0; // pair pipeline: filter tiles (n_tiles counts walk units of kSuper of them)
 };
 
 Launch plan(const DeviceTrie& dt, uint64_t n_own)
 {
     Launch l;
     l.n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
+    if (dt.pair) {
+        l.n_ftiles = l.n_tiles;
+        l.n_tiles = (l.n_ftiles + gpu::kSuper - 1) / gpu::kSuper;
+    }
     l.grid = std::min<uint64_t>(uint64_t(dt.sm_count) * dt.blocks_per_sm,
-                                std::max<uint64_t>(1, (l.n_tiles + gpu::kWarps - 1) / gpu::kWarps));
-    l.warps = l.grid * gpu::kWarps;
+                                std::max<uint64_t>(1, (l.n_tiles + dt.warps - 1) / dt.warps));
+    l.warps = l.grid * dt.warps;
     return l;
 }
 
@@ -412,14 +472,44 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
     a.base_out = base_out;
     a.warp_need = ws.d_small;
     a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
+    if (dt.pair) {
+        const uint64_t fgrid = uint64_t(dt.sm_count) * dt.filter_blocks_per_sm;
+        const uint64_t fwarps = fgrid * gpu::kFWarps;
+        ws.ensure_ctiles(l.n_ftiles);
+        // expected: ~0.2% of starts survive; regions grow on overflow
+        if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / 256 / fwarps + 256);
+        ws.ensure_cand(fwarps, ws.cand_cap);
+        gpu::FilterArgs f{};
+        f.table = dt.view.filter;
+        f.table_words = dt.view.filter_words;
+        f.pair_shift = dt.view.pair_shift;
+        f.text = d_text;
+        f.n_avail = n_avail;
+        const uint64_t me = dt.min_emit;
+        f.start_end = n_avail >= me ? std::min(n_own, n_avail - me + 1) : 0;
+        f.n_tiles = l.n_ftiles;
+        f.cand = ws.d_cand;
+        f.cand_cap = ws.cand_cap;
+        f.tile_ccount = ws.d_tile_ccount;
+        f.tile_cslot = ws.d_tile_cslot;
+        f.cand_need = ws.d_small + 5;
+        gpu::pfac_pair_filter_kernel<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
+        CK(cudaGetLastError());
+        a.cand = ws.d_cand;
+        a.cand_cap = ws.cand_cap;
+        a.tile_ccount = ws.d_tile_ccount;
+        a.tile_cslot = ws.d_tile_cslot;
+        a.cand_warps = uint32_t(fwarps);
+        a.n_ftiles = l.n_ftiles;
+    }
     void* params[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(l.grid)),
-                                                      dim3(gpu::kThreads), params, dt.smem, ws.stream);
+                                                      dim3(dt.warps * 32), params, dt.smem, ws.stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         cuda_fail(e, "pfac_scan_kernel launch");
     }
-    return 1;
+    return dt.pair ? 2 : 1;
 }
 
 // Reads back the scan's accumulators; true when the results are complete.
@@ -429,12 +519,19 @@ bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own, const unsi
     if (!records) records = ws.d_small + 4;
     CK(cudaMemcpyAsync(ws.h_small, ws.d_small, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaMemcpyAsync(ws.h_small + 4, records, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(ws.h_small + 5, ws.d_small + 5, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
     if (ws.h_small[2] & 1u) fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
     bool ok = true;
     if (ws.h_small[0]) { // some warp's staging region overflowed
         const Launch l = plan(dt, n_own);
         ws.ensure_stage(l.warps, ws.h_small[0] + ws.h_small[0] / 4 + 64);
+        ok = false;
+    }
+    if (ws.h_small[5]) { // some filter warp's candidate region overflowed
+        const uint64_t fwarps = uint64_t(dt.sm_count) * dt.filter_blocks_per_sm * gpu::kFWarps;
+        ws.ensure_cand(fwarps, ws.h_small[5] + ws.h_small[5] / 4 + 256);
         ok = false;
     }
     if (ws.h_small[4] > ws.out_cap) {

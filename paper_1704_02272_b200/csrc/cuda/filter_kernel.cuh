@@ -1,0 +1,230 @@
+// filter_kernel.cuh -- the lean first pass of the pair-filter scan pipeline.
+//
+// Reference semantics: none of its own -- it only discards start offsets that
+// cannot report (a conservative pre-filter of scan.cpp:82-87, where every
+// offset starts a walk).  Every start that survives is walked by the second
+// pass (pfac_scan_kernel<..., CANDS = true>), which produces the records.
+//
+// Why a separate kernel: the filter needs ~50 registers, the walk ~120.  In
+// one kernel the walk's register budget caps the SM at 16 warps, and the
+// filter (random shared-memory probes, short dependent chains) is latency
+// bound at 16 warps.  Alone it runs 32 warps per SM.
+//
+// Work decomposition (tiles as in scan_kernel.cuh: 8192 starts, round-robin
+// over warps).  A warp takes a tile in steps of kFChunks 512-byte chunks:
+//   - each lane owns 16 consecutive starts of each chunk (one 16-byte LDG,
+//     the 4 overhang bytes from the next lane by SHFL), coalesced 512 B per
+//     warp instruction, the next step prefetched into registers;
+//   - first level: the pair filter (layout.hpp, 8 shared-memory probes per 16
+//     starts), giving a 16-bit mask per chunk;
+//   - second level, batched over the step: the lane's text goes to a per-warp
+//     staging area in shared memory, one warp scan places the candidates in
+//     start order in a queue, and full 32-lane rounds test each candidate's
+//     other role; survivors are appended, still in start order, to the warp's
+//     region of the candidate buffer (u16 tile-relative offsets).
+//   - per tile: survivor count and the slot of its first survivor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "layout.hpp"
+
+namespace hfb::gpu {
+
+#ifndef HFB_FWARPS
+#define HFB_FWARPS 32
+#endif
+constexpr uint32_t kFWarps = HFB_FWARPS;
+constexpr uint32_t kFThreads = kFWarps * 32;
+constexpr uint32_t kFChunk = 512;                     // bytes per warp chunk (16 per lane)
+constexpr uint32_t kFChunks = 4;                      // chunks per step
+constexpr uint32_t kFStep = kFChunk * kFChunks;       // 2 KiB
+constexpr uint32_t kFStageStride = kFChunk + 16;      // staged chunk + overhang, 16-aligned
+constexpr uint32_t kFQueue = 512;                     // candidate queue entries (>= one chunk)
+constexpr uint32_t kFWarpSmem = kFChunks * kFStageStride + kFQueue * 2;
+constexpr uint32_t kFTile = 8192;                     // == kTile of scan_kernel.cuh
+
+struct FilterArgs {
+    const uint32_t* table;   // pair table, 2^wb words
+    uint32_t table_words;
+    uint32_t pair_shift;     // 32 - wb
+    const uint8_t* text;     // 16-byte aligned, readable up to round_up(n_avail, 16) + 16
+    uint64_t n_avail;        // bytes of text
+    uint64_t start_end;      // starts [0, start_end) may report
+    uint64_t n_tiles;
+    uint16_t* cand;          // gridDim.x * kFWarps regions of cand_cap entries
+    uint64_t cand_cap;
+    uint32_t* tile_ccount;
+    uint32_t* tile_cslot;
+    unsigned long long* cand_need; // max entries any warp needed (overflow sizing)
+};
+
+__device__ __forceinline__ uint32_t f_lds(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// First level over one 16-start lane slice: w[0..3] its bytes, w[4] the next 4.
+// Bit j = start j passed its first role (layout.hpp, pair form).
+__device__ __forceinline__ uint32_t f_pair_level1(const uint32_t (&w)[5], uint32_t tbase, uint32_t shift)
+{
+    uint32_t m0 = 0, m1 = 0; // two independent chains, MSB-first
+#pragma unroll
+    for (int i = 1; i < 16; i += 2) {
+        auto win = [&](int n) -> uint32_t {
+            return (n & 3) ? __funnelshift_r(w[n >> 2], w[(n >> 2) + 1], 8 * (n & 3)) : w[n >> 2];
+        };
+        const uint32_t mid = win(i), a = win(i - 1), b = win(i + 3);
+        const uint32_t word = f_lds(tbase + (((mid * kPairMul) >> shift) << 2));
+        uint32_t& m = i < 8 ? m0 : m1;
+        m = __funnelshift_l(__funnelshift_l(0u, word, a), m, 1); // start i - 1 (role A)
+        m = __funnelshift_l(__funnelshift_l(0u, word, b), m, 1); // start i (role B)
+    }
+    return __brev((m0 << 24) | (m1 << 16)); // start j at bit j
+}
+
+__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __grid_constant__ FilterArgs a)
+{
+    extern __shared__ __align__(128) uint8_t fsmem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
+    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
+    __syncthreads();
+    const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+    uint8_t* stage = fsmem + size_t(a.table_words) * 4 + warp * kFWarpSmem;
+    uint16_t* q = reinterpret_cast<uint16_t*>(stage + kFChunks * kFStageStride);
+    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+
+    const uint32_t gw = blockIdx.x * kFWarps + warp, W = gridDim.x * kFWarps;
+    const uint32_t shift = a.pair_shift;
+    const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
+    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
+    uint64_t cursor = 0;
+    const uint32_t below = (1u << lane) - 1u;
+
+    // 16 bytes of lane `lane` of chunk at text offset `at` (zeros past the buffer)
+    auto load = [&](uint64_t at) -> uint4 {
+        const uint64_t p = at + 16u * lane;
+        return p < avail16 ? __ldg(reinterpret_cast<const uint4*>(a.text + p)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+
+    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
+        const uint64_t lo = tile * kFTile;
+        const uint64_t slot = cursor;
+        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
+        const uint32_t steps = (rem + kFStep - 1) / kFStep;
+        uint4 nxt[kFChunks];
+        if (steps) {
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(lo + b * kFChunk);
+        }
+        for (uint32_t s = 0; s < steps; ++s) {
+            const uint64_t sbase = lo + uint64_t(s) * kFStep;
+            uint4 cur[kFChunks];
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
+            if (s + 1 < steps) {
+#pragma unroll
+                for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(sbase + kFStep + b * kFChunk);
+            }
+            // lane 31's overhang of the last chunk: the first word after the step
+            uint32_t tail = 0;
+            if (lane == 31 && sbase + kFStep < avail16)
+                tail = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
+
+            uint32_t mask[kFChunks];
+            uint32_t packed_lo = 0, packed_hi = 0; // survivor counts, 16 bits per chunk
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) {
+                const uint32_t from_next = __shfl_sync(0xFFFFFFFFu, cur[(b + 1) % kFChunks].x, 0);
+                uint32_t ov = __shfl_sync(0xFFFFFFFFu, cur[b].x, (lane + 1) & 31u);
+                if (lane == 31) ov = b + 1 < kFChunks ? from_next : tail;
+                // stage the slice for the second level
+                *reinterpret_cast<uint4*>(stage + b * kFStageStride + 16u * lane) = cur[b];
+                if (lane == 31) *reinterpret_cast<uint32_t*>(stage + b * kFStageStride + kFChunk) = ov;
+                const uint32_t w[5] = {cur[b].x, cur[b].y, cur[b].z, cur[b].w, ov};
+                const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
+                const uint32_t valid = r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+                mask[b] = f_pair_level1(w, tbase, shift) & valid;
+                const uint32_t c = uint32_t(__popc(mask[b]));
+                if (b < 2) packed_lo |= c << (16 * b);
+                else packed_hi |= c << (16 * (b - 2));
+            }
+            if (!__any_sync(0xFFFFFFFFu, packed_lo | packed_hi)) continue;
+            __syncwarp(); // staged text visible to the whole warp
+            // one scan per pair of chunks (16-bit fields never carry)
+            uint32_t inc_lo = packed_lo, inc_hi = packed_hi;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t ul = __shfl_up_sync(0xFFFFFFFFu, inc_lo, d);
+                const uint32_t uh = __shfl_up_sync(0xFFFFFFFFu, inc_hi, d);
+                if (lane >= uint32_t(d)) inc_lo += ul, inc_hi += uh;
+            }
+            const uint32_t tot_lo = __shfl_sync(0xFFFFFFFFu, inc_lo, 31);
+            const uint32_t tot_hi = __shfl_sync(0xFFFFFFFFu, inc_hi, 31);
+            uint32_t ex[kFChunks], tot[kFChunks];
+            ex[0] = (inc_lo - packed_lo) & 0xFFFFu, ex[1] = (inc_lo - packed_lo) >> 16;
+            ex[2] = (inc_hi - packed_hi) & 0xFFFFu, ex[3] = (inc_hi - packed_hi) >> 16;
+            tot[0] = tot_lo & 0xFFFFu, tot[1] = tot_lo >> 16, tot[2] = tot_hi & 0xFFFFu, tot[3] = tot_hi >> 16;
+            const uint32_t all = tot[0] + tot[1] + tot[2] + tot[3];
+
+            // Queue chunks [b0, b1) (their candidates fit), then test them in
+            // full rounds and append the survivors to the region.
+            auto run = [&](uint32_t b0, uint32_t b1) {
+                uint32_t base = 0;
+#pragma unroll
+                for (uint32_t b = 0; b < kFChunks; ++b) {
+                    if (b < b0 || b >= b1) continue;
+                    uint32_t at = base + ex[b];
+                    const uint32_t first = s * kFStep + b * kFChunk + 16u * lane;
+                    for (uint32_t m = mask[b]; m; m &= m - 1) q[at++] = uint16_t(first + __ffs(m) - 1);
+                    base += tot[b];
+                }
+                __syncwarp();
+                for (uint32_t r0 = 0; r0 < base; r0 += 32) {
+                    const uint32_t e = r0 + lane;
+                    uint32_t off = 0;
+                    bool keep = false;
+                    if (e < base) {
+                        off = q[e]; // tile-relative start
+                        const uint32_t in_step = off - s * kFStep;
+                        const uint32_t sa = stage_s + (in_step >> 9) * kFStageStride + (in_step & (kFChunk - 1));
+                        uint32_t lo4, hi4;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo4) : "r"(sa & ~3u));
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi4) : "r"((sa & ~3u) + 4));
+                        const uint32_t y = __funnelshift_r(lo4, hi4, 8 * (sa & 3u)); // bytes off..off+3
+                        const bool odd = off & 1u;
+                        const uint32_t mid = odd ? (y >> 8) : y;
+                        const uint32_t amt = odd ? y : (y >> 24);
+                        const uint32_t word = f_lds(tbase + (((mid * kPairMul) >> shift) << 2));
+                        keep = int32_t(word << (amt & 31u)) < 0;
+                    }
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                    if (keep) {
+                        const uint64_t at = cursor + __popc(bal & below);
+                        if (at < a.cand_cap) region[at] = uint16_t(off);
+                    }
+                    cursor += __popc(bal);
+                }
+                __syncwarp(); // queue reads done before the next writes
+            };
+            if (all <= kFQueue) {
+                run(0, kFChunks);
+            } else {
+                for (uint32_t b = 0; b < kFChunks; ++b)
+                    if (tot[b]) run(b, b + 1);
+            }
+        }
+        if (lane == 0) {
+            a.tile_ccount[tile] = uint32_t(cursor - slot);
+            a.tile_cslot[tile] = uint32_t(slot);
+        }
+    }
+    if (lane == 0 && cursor > a.cand_cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+}
+
+constexpr uint32_t filter_smem_fixed_bytes() { return kFWarps * kFWarpSmem; }
+
+} // namespace hfb::gpu

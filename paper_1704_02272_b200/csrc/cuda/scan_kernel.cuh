@@ -47,11 +47,22 @@ namespace cg = cooperative_groups;
 #endif
 constexpr uint32_t kWarps = HFB_WARPS; // warps per CTA (one CTA per SM)
 constexpr uint32_t kThreads = kWarps * 32;
-constexpr uint32_t kLaneStarts = 32;                 // consecutive starts per lane per group
+#ifndef HFB_CWARPS
+#define HFB_CWARPS 32
+#endif
+constexpr uint32_t kCWarps = HFB_CWARPS; // warps per CTA of the candidate-walking pass (CANDS)
+constexpr uint32_t kSliceStarts = 16;                // consecutive starts of one lane slice
+constexpr uint32_t kSlices = 2;                       // slices per lane per group
+constexpr uint32_t kLaneStarts = kSliceStarts * kSlices;
 constexpr uint32_t kGroup = 32 * kLaneStarts;         // 1024 starts per warp group
+constexpr uint32_t kSliceSpan = 32 * kSliceStarts;    // slice s of lane L = group bytes [s*512 + 16L, +16)
 constexpr uint32_t kGroupsPerTile = 8;
 constexpr uint32_t kTile = kGroup * kGroupsPerTile;   // 8192 starts per warp-tile
-constexpr uint32_t kQueue = kGroup;                   // per-warp candidate queue (tile offsets)
+constexpr uint32_t kSuper = 8;                        // CANDS walk unit: 8 tiles (u16 offsets still fit)
+#ifndef HFB_QUEUE
+#define HFB_QUEUE 1024
+#endif
+constexpr uint32_t kQueue = HFB_QUEUE;                // per-warp candidate queue (tile offsets), >= kGroup
 constexpr uint32_t kStages = HFB_STAGES;              // per-warp TMA ring depth (groups in flight)
 constexpr uint32_t kStageBytes = kGroup + 16;         // a group + the key overhang, 16-aligned
 constexpr uint32_t kRegRecords = 2;                   // records a lane keeps per walk round
@@ -75,6 +86,13 @@ struct ScanArgs {
     unsigned long long* base_out;      // base_in + this launch's total (distinct word)
     unsigned long long* warp_need;     // max records any warp needed (overflow sizing)
     unsigned int* err;
+    // CANDS launches: per-tile start candidates from pfac_pair_filter_kernel
+    const uint16_t* cand;       // cand_warps regions of cand_cap tile-relative offsets
+    uint64_t cand_cap;
+    const uint32_t* tile_ccount;
+    const uint32_t* tile_cslot;
+    uint32_t cand_warps;        // tile t's candidates live in region t % cand_warps
+    uint64_t n_ftiles;          // filter tiles; n_tiles then counts walk units of kSuper tiles
 };
 
 // ---- text and dictionary helpers --------------------------------------------------
@@ -229,10 +247,10 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
 
 // ---- start filter ------------------------------------------------------------
 
-// Bit j set = start j of this lane's 32 may report.  w[0..9] = the lane's
-// 32 bytes plus the next 8.  KW: 1 = k < 4, 2 = k in 5..8, 3 = k == 4.
+// Bit j set = start j of the lane slice may report.  w[0..5] = the slice's
+// 16 bytes plus the next 8.  KW: 1 = k < 4, 2 = k in 5..8, 3 = k == 4.
 template <int KW>
-__device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_t (&w)[10], const uint32_t* s_filter,
+__device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_t (&w)[6], const uint32_t* s_filter,
                                                 uint32_t valid)
 {
     if (KW == 0) return valid;
@@ -241,9 +259,9 @@ __device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_
     const uint32_t m32 = (KW == 3 || k >= 4) ? 0xFFFFFFFFu : ((1u << (8 * k)) - 1u);
     const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
     const uint8_t* fbytes = reinterpret_cast<const uint8_t*>(s_filter);
-    uint32_t m = 0; // start j ends up at bit 31 - j
+    uint32_t m[2] = {0u, 0u}; // start j ends up at bit 7 - j % 8 of m[j / 8]
 #pragma unroll
-    for (int j = 0; j < int(kLaneStarts); ++j) {
+    for (int j = 0; j < int(kSliceStarts); ++j) {
         const uint32_t lo = (j & 3) ? __funnelshift_r(w[j >> 2], w[(j >> 2) + 1], 8 * (j & 3)) : w[j >> 2];
         uint32_t key;
         if (KW == 2) {
@@ -255,14 +273,13 @@ __device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_
         }
         const uint32_t off = __umulhi(key, kFilterMul) & mask4; // filter_word(key) * 4
         const uint32_t word = *reinterpret_cast<const uint32_t*>(fbytes + off);
-        m = __funnelshift_l(__funnelshift_l(0u, word, key), m, 1); // (m << 1) | bit (key & 31), MSB-first
+        m[j >> 3] = __funnelshift_l(__funnelshift_l(0u, word, key), m[j >> 3], 1); // MSB-first
     }
-    return __brev(m) & valid; // start j at bit j
+    return (__brev((m[0] << 24) | (m[1] << 16))) & valid; // start j at bit j
 }
 
 // 32-bit word at byte offset `off` of dynamic shared memory (the start
-// filter table lives at offset 0).  Addressing the symbol directly lets ptxas
-// fold its window offset into the LDS immediate.
+// filter table lives at offset 0).
 __device__ __forceinline__ uint32_t table_word(uint32_t off)
 {
     uint32_t v;
@@ -276,38 +293,92 @@ __device__ __forceinline__ uint32_t table_word(uint32_t off)
 // the word of the middle at odd position i = 2p + 1 and tests start i - 1
 // (role A: bit of its first byte) and start i (role B: bit of its 4th byte).
 // Returns bit j = start j passed its first role.
-__device__ __forceinline__ uint32_t filter_pair(const uint32_t (&w)[10], uint32_t shift, uint32_t valid)
+#ifndef HFB_CHAINS
+#define HFB_CHAINS 4 // independent mask accumulators in the pair filter
+#endif
+#ifndef HFB_HASHHI
+#define HFB_HASHHI 0 // pair hash shift as IMAD.HI (FMA pipe) instead of SHF (ALU pipe)
+#endif
+#ifndef HFB_WINHI
+#define HFB_WINHI 0 // in-word windows as IMAD.HI instead of funnel shifts
+#endif
+
+__device__ __forceinline__ uint32_t pair_offset(const TrieView& t, uint32_t mid)
 {
-    uint32_t m = 0; // start j ends up at bit 31 - j
+    const uint32_t h = mid * kPairMul;
+    return (HFB_HASHHI ? __umulhi(h, t.pair_mul) : (h >> t.pair_shift)) << 2; // pair_word(mid) * 4
+}
+
+__device__ __forceinline__ uint32_t filter_pair(const TrieView& t, const uint32_t (&w)[5], uint32_t valid)
+{
+    // Windows at 4q+1 (x >> 8) and 4q+2 (x >> 16) may come off the FMA pipe
+    // as high multiplies; those spanning two words are ALU funnel shifts.
+    // Only the low 24 bits of a middle and the low 5 of an amount matter.
+    auto window = [&](int n) -> uint32_t {
+        switch (n & 3) {
+        case 0: return w[n >> 2];
+        case 1: return HFB_WINHI ? __umulhi(w[n >> 2], t.mul_shr8) : (w[n >> 2] >> 8);
+        case 2: return HFB_WINHI ? __umulhi(w[n >> 2], t.mul_shr16) : (w[n >> 2] >> 16);
+        default: return __funnelshift_r(w[n >> 2], w[(n >> 2) + 1], 24);
+        }
+    };
+    // independent accumulators keep the dependent funnel-shift chains short
+    constexpr int kChains = HFB_CHAINS > 2 ? 2 : HFB_CHAINS;
+    constexpr int kPer = int(kSliceStarts) / kChains;
+    uint32_t m[kChains];
 #pragma unroll
-    for (int i = 1; i < int(kLaneStarts); i += 2) {
-        // window(n) = text bytes n..n+3 of the lane slice
-        const uint32_t mid = __funnelshift_r(w[i >> 2], w[(i >> 2) + 1], 8 * (i & 3));
-        const int a = i - 1, b = i + 3; // even positions
-        const uint32_t amt_a = (a & 3) ? __funnelshift_r(w[a >> 2], w[(a >> 2) + 1], 16) : w[a >> 2];
-        const uint32_t amt_b = (b & 3) ? __funnelshift_r(w[b >> 2], w[(b >> 2) + 1], 16) : w[b >> 2];
-        const uint32_t word = table_word(((mid * kPairMul) >> shift) << 2); // pair_word(mid) * 4
-        m = __funnelshift_l(__funnelshift_l(0u, word, amt_a), m, 1); // start i - 1
-        m = __funnelshift_l(__funnelshift_l(0u, word, amt_b), m, 1); // start i
+    for (int c = 0; c < kChains; ++c) m[c] = 0u;
+#pragma unroll
+    for (int i = 1; i < int(kSliceStarts); i += 2) {
+        const uint32_t mid = window(i);
+        const uint32_t amt_a = window(i - 1), amt_b = window(i + 3);
+        const uint32_t word = table_word(pair_offset(t, mid));
+        uint32_t& acc = m[i / kPer];
+        acc = __funnelshift_l(__funnelshift_l(0u, word, amt_a), acc, 1); // start i - 1
+        acc = __funnelshift_l(__funnelshift_l(0u, word, amt_b), acc, 1); // start i
     }
-    return __brev(m) & valid;
+    uint32_t msb_first = 0; // start j at bit 31 - j
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) msb_first |= m[c] << (32 - kPer * (c + 1));
+    return __brev(msb_first) & valid;
 }
 
 // Second pair level: each survivor j of `mask` tests its other role (odd j:
 // role A at the middle j + 1; even j: role B at the middle j), reading its 4
-// bytes back from the staged lane slice `src` in shared memory.
-__device__ __forceinline__ uint32_t filter_pair_second(uint32_t mask, const uint8_t* src, uint32_t shift)
+// bytes back from the staged lane slice `src` in shared memory.  Two
+// survivors (the lowest and the highest) per round for latency overlap.
+#ifndef HFB_L2PAIR
+#define HFB_L2PAIR 1 // second level handles two survivors per round
+#endif
+
+__device__ __forceinline__ bool pair_second_test(const TrieView& t, const uint8_t* src, uint32_t j)
 {
-    uint32_t keep = 0;
-    for (uint32_t c = mask; c; c &= c - 1) {
-        const uint32_t j = __ffs(c) - 1;
-        const uint32_t* wp = reinterpret_cast<const uint32_t*>(src + (j & ~3u));
-        const uint32_t y = __funnelshift_r(wp[0], wp[1], 8 * (j & 3)); // bytes j..j+3
-        const bool odd = j & 1u;
-        const uint32_t mid = odd ? (y >> 8) : y;
-        const uint32_t amt = odd ? y : (y >> 24);
-        const uint32_t word = table_word(((mid * kPairMul) >> shift) << 2);
-        keep |= ((word << (amt & 31u)) >> 31) << j;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(src + (j & ~3u));
+    const uint32_t y = __funnelshift_r(wp[0], wp[1], 8 * j); // bytes j..j+3 (shift wraps mod 32)
+    const bool odd = j & 1u;
+    const uint32_t mid = odd ? (y >> 8) : y;
+    const uint32_t amt = odd ? y : (y >> 24);
+    const uint32_t word = table_word(pair_offset(t, mid));
+    return int32_t(word << (amt & 31u)) < 0;
+}
+
+__device__ __forceinline__ uint32_t filter_pair_second(const TrieView& t, uint32_t mask, const uint8_t* src)
+{
+    uint32_t keep = mask;
+    if (HFB_L2PAIR) {
+        for (uint32_t c = mask; c;) {
+            const uint32_t lo = __ffs(c) - 1, hi = 31 - __clz(c);
+            c &= ~((1u << lo) | (1u << hi));
+            const bool ok_lo = pair_second_test(t, src, lo);
+            const bool ok_hi = pair_second_test(t, src, hi);
+            if (!ok_lo) keep &= ~(1u << lo);
+            if (!ok_hi) keep &= ~(1u << hi);
+        }
+    } else {
+        for (uint32_t c = mask; c; c &= c - 1) {
+            const uint32_t j = __ffs(c) - 1;
+            if (!pair_second_test(t, src, j)) keep &= ~(1u << j);
+        }
     }
     return keep;
 }
@@ -326,6 +397,7 @@ __device__ __forceinline__ uint32_t warp_exclusive(uint32_t v, uint32_t lane, ui
     return incl - v;
 }
 
+template <uint32_t NW>
 __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr, uint32_t& total)
 {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -334,14 +406,14 @@ __device__ __forceinline__ uint32_t block_exclusive(uint32_t v, uint32_t* s_scr,
     if (lane == 0) s_scr[warp] = wt;
     __syncthreads();
     if (warp == 0) {
-        const uint32_t x = lane < kWarps ? s_scr[lane] : 0u;
+        const uint32_t x = lane < NW ? s_scr[lane] : 0u;
         uint32_t tt;
         const uint32_t xe = warp_exclusive(x, lane, tt);
-        if (lane < kWarps) s_scr[lane] = xe;
-        if (lane == 0) s_scr[kWarps] = tt;
+        if (lane < NW) s_scr[lane] = xe;
+        if (lane == 0) s_scr[NW] = tt;
     }
     __syncthreads();
-    total = s_scr[kWarps];
+    total = s_scr[NW];
     const uint32_t r = s_scr[warp] + ex;
     __syncthreads();
     return r;
@@ -394,7 +466,14 @@ struct Walker {
 
     // Candidates [0, n) of the tile starting at `lo`: second-level probe,
     // then walk the survivors and append their records in start order.
+#ifndef HFB_FLUSH_NOINLINE
+#define HFB_FLUSH_NOINLINE 0
+#endif
+#if HFB_FLUSH_NOINLINE
+    __device__ __noinline__ void flush(uint64_t lo, uint32_t n)
+#else
     __device__ __forceinline__ void flush(uint64_t lo, uint32_t n)
+#endif
     {
         uint32_t ns = n;
         if (KW != 0 && a.trie.filter2_bits) {
@@ -487,32 +566,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 }
 
 // Shared-memory bytes a CTA needs beyond the filter bitmap.
-constexpr uint32_t smem_fixed_bytes() { return kWarps * kStages * kStageBytes + kWarps * kQueue * 2 + 512; }
-
-template <bool GROUPED, bool IDENT, int KW, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a)
+constexpr uint32_t smem_fixed_bytes(bool cands)
 {
+    return cands ? kCWarps * kQueue * 2 + 512 : kWarps * kStages * kStageBytes + kWarps * kQueue * 2 + 512;
+}
+
+// CANDS = false: the fused scan (filter, walks, ordered output) over text.
+// CANDS = true: the second pass of the pair pipeline -- walks the candidates
+// pfac_pair_filter_kernel left per tile; no filter, no text staging.
+template <bool GROUPED, bool IDENT, int KW, bool PAIR, bool CANDS = false>
+__global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_kernel(const __grid_constant__ ScanArgs a)
+{
+    constexpr uint32_t NW = CANDS ? kCWarps : kWarps, NT = NW * 32;
     extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t fwords = KW ? a.trie.filter_words : 0u;
+    const uint32_t fwords = (KW && !CANDS) ? a.trie.filter_words : 0u;
     uint32_t* s_filter = reinterpret_cast<uint32_t*>(smem);                   // first: 2^bits / 8 bytes
     uint8_t* s_ring = smem + size_t(fwords) * 4;                               // [warp][stage][kStageBytes]
-    uint16_t* s_queue = reinterpret_cast<uint16_t*>(s_ring + kWarps * kStages * kStageBytes);
-    uint16_t* s_sym = s_queue + kWarps * kQueue;                               // [256]
-    __shared__ uint64_t s_bar[kWarps][kStages];
-    __shared__ uint32_t s_scr[kWarps + 1];
+    uint16_t* s_queue = reinterpret_cast<uint16_t*>(s_ring + (CANDS ? 0u : NW * kStages * kStageBytes));
+    uint16_t* s_sym = s_queue + NW * kQueue;                                   // [256]
+    __shared__ uint64_t s_bar[CANDS ? 1 : NW][kStages];
+    __shared__ uint32_t s_scr[NW + 1];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const TrieView& t = a.trie;
-    for (uint32_t i = tid; i < fwords; i += kThreads) s_filter[i] = __ldg(t.filter + i);
+    for (uint32_t i = tid; i < fwords; i += NT) s_filter[i] = __ldg(t.filter + i);
     if (!IDENT)
-        for (uint32_t i = tid; i < 256; i += kThreads) s_sym[i] = __ldg(t.symtab + i);
+        for (uint32_t i = tid; i < 256; i += NT) s_sym[i] = __ldg(t.symtab + i);
 
     const uint64_t me = t.min_emit;
     const uint64_t start_end = a.n_avail >= me ? min(a.n_own, a.n_avail - me + 1) : 0;
     const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
-    const uint32_t gw = blockIdx.x * kWarps + warp, W = gridDim.x * kWarps;
+    const uint32_t gw = blockIdx.x * NW + warp, W = gridDim.x * NW;
     uint8_t* ring = s_ring + warp * kStages * kStageBytes;
-    uint64_t* bars = s_bar[warp];
+    uint64_t* bars = s_bar[CANDS ? 0 : warp];
 
     // Producer (lane 0): the warp's groups -- tiles gw, gw + W, ..., 8 groups
     // each, up to `stop` -- with kStages in flight.  The consumer below visits
@@ -529,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         p_addr += kGroup;
         if (++p_g == kGroupsPerTile) p_g = 0, p_addr += p_skip;
     };
-    if (lane == 0) {
+    if (lane == 0 && !CANDS) {
         for (uint32_t s = 0; s < kStages; ++s) mbar_init(&bars[s]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t s = 0; s < kStages; ++s) produce();
@@ -537,8 +623,47 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     __syncthreads(); // filter, symbol map and barrier inits visible
 
     Walker<GROUPED, IDENT, KW> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
+    if constexpr (CANDS) {
+        // Walk units of kSuper filter tiles: lane i < kSuper fetches tile i's
+        // candidate count and slot, so one load latency covers the unit, and
+        // rounds are filled across tile boundaries.
+        for (uint64_t unit = gw; unit < a.n_tiles; unit += W) {
+            const uint64_t lo = unit * uint64_t(kSuper) * kTile;
+            const uint64_t slot = wk.cursor;
+            const uint64_t ft = unit * kSuper + lane;
+            uint32_t cnt = 0, cslot = 0;
+            if (lane < kSuper && ft < a.n_ftiles) cnt = a.tile_ccount[ft], cslot = a.tile_cslot[ft];
+            uint32_t qn = 0;
+            for (uint32_t i = 0; i < kSuper; ++i) {
+                const uint32_t n_i = __shfl_sync(0xFFFFFFFFu, cnt, i);
+                if (n_i == 0) continue;
+                const uint32_t s_i = __shfl_sync(0xFFFFFFFFu, cslot, i);
+                const uint64_t t_i = unit * kSuper + i;
+                const uint16_t* src = a.cand + (t_i % a.cand_warps) * a.cand_cap + s_i;
+                for (uint32_t c0 = 0; c0 < n_i;) {
+                    if (qn == kQueue) {
+                        __syncwarp();
+                        wk.flush(lo, qn);
+                        qn = 0;
+                    }
+                    const uint32_t n = min(kQueue - qn, n_i - c0);
+                    for (uint32_t k = lane; k < n; k += 32) wk.q[qn + k] = uint16_t(src[c0 + k] + i * kTile);
+                    qn += n;
+                    c0 += n;
+                }
+            }
+            if (qn) {
+                __syncwarp();
+                wk.flush(lo, qn);
+            }
+            if (lane == 0) {
+                a.tile_count[unit] = uint32_t(wk.cursor - slot);
+                a.tile_slot[unit] = uint32_t(slot);
+            }
+        }
+    }
     uint32_t c_stage = 0, c_parity = 0;
-    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
+    for (uint64_t tile = gw; !CANDS && tile < a.n_tiles; tile += W) {
         const uint64_t lo = tile * kTile;
         const uint64_t slot = wk.cursor;
         // tile-relative limits (32-bit): starts that may report, groups fetched
@@ -546,36 +671,73 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         const uint32_t fetched = uint32_t(min((stop - lo + kGroup - 1) / kGroup, uint64_t(kGroupsPerTile)));
         uint32_t qn = 0;
         for (uint32_t g = 0; g < fetched; ++g) {
-            const int32_t r = int32_t(rem) - int32_t(g * kGroup + lane * kLaneStarts);
-            const uint32_t valid = r >= int32_t(kLaneStarts) ? 0xFFFFFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            // slice s of this lane: group starts [s * 512 + 16 * lane, +16)
+            uint32_t valid[kSlices];
+#pragma unroll
+            for (uint32_t sl = 0; sl < kSlices; ++sl) {
+                const int32_t r = int32_t(rem) - int32_t(g * kGroup + sl * kSliceSpan + lane * kSliceStarts);
+                valid[sl] = r >= int32_t(kSliceStarts) ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            }
             mbar_wait(&bars[c_stage], c_parity);
-            uint32_t mask = 0;
-            if (__any_sync(0xFFFFFFFFu, valid)) {
-                const uint8_t* src = ring + c_stage * kStageBytes + lane * kLaneStarts;
-                const uint4 v0 = *reinterpret_cast<const uint4*>(src);
-                const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
-                const uint2 x = *reinterpret_cast<const uint2*>(src + 32);
-                const uint32_t w[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, x.x, x.y};
+            uint32_t mask[kSlices] = {};
+            if (__any_sync(0xFFFFFFFFu, valid[0] | valid[kSlices - 1])) {
+                // Conflict-free 16-byte reads (a quarter-warp covers 128
+                // contiguous bytes); each slice's overhang comes from the next
+                // lane, the last lane's from lane 0's next slice or the tail.
+                const uint8_t* stage = ring + c_stage * kStageBytes;
+                uint4 v[kSlices];
+#pragma unroll
+                for (uint32_t sl = 0; sl < kSlices; ++sl)
+                    v[sl] = *reinterpret_cast<const uint4*>(stage + sl * kSliceSpan + lane * kSliceStarts);
+                const uint2 tail = *reinterpret_cast<const uint2*>(stage + kGroup);
+                const uint32_t nxt = (lane + 1) & 31u;
+#pragma unroll
+                for (uint32_t sl = 0; sl < kSlices; ++sl) {
+                    const bool last = sl + 1 == kSlices;
+                    const uint32_t sx = (lane == 0 && !last) ? v[sl + 1].x : v[sl].x;
+                    const uint32_t sy = (lane == 0 && !last) ? v[sl + 1].y : v[sl].y;
+                    uint32_t ox = __shfl_sync(0xFFFFFFFFu, sx, nxt);
+                    uint32_t oy = __shfl_sync(0xFFFFFFFFu, sy, nxt);
+                    if (last && lane == 31) ox = tail.x, oy = tail.y;
+                    if (PAIR) {
+                        const uint32_t w[5] = {v[sl].x, v[sl].y, v[sl].z, v[sl].w, ox};
+                        mask[sl] = filter_pair(t, w, valid[sl]);
+                    } else {
+                        const uint32_t w[6] = {v[sl].x, v[sl].y, v[sl].z, v[sl].w, ox, oy};
+                        mask[sl] = filter_mask<KW>(t, w, s_filter, valid[sl]);
+                    }
+                }
                 if (PAIR) {
-                    mask = filter_pair(w, t.pair_shift, valid);
-                    mask = filter_pair_second(mask, src, t.pair_shift);
-                } else {
-                    mask = filter_mask<KW>(t, w, s_filter, valid);
+#pragma unroll
+                    for (uint32_t sl = 0; sl < kSlices; ++sl)
+                        mask[sl] = filter_pair_second(t, mask[sl], stage + sl * kSliceSpan + lane * kSliceStarts);
                 }
             }
             __syncwarp();
             if (lane == 0) produce(); // the stage is consumed: refill it
             if (++c_stage == kStages) c_stage = 0, c_parity ^= 1u;
-            if (__any_sync(0xFFFFFFFFu, mask)) { // queue the candidates, in start order
-                uint32_t tot;
-                const uint32_t ex = warp_exclusive(__popc(mask), lane, tot);
+            static_assert(kSlices == 2, "survivor counts pack into two 16-bit fields");
+            uint32_t packed = 0; // per-slice survivor counts, 16 bits each
+#pragma unroll
+            for (uint32_t sl = 0; sl < kSlices; ++sl) packed |= uint32_t(__popc(mask[sl])) << (16 * sl);
+            if (__any_sync(0xFFFFFFFFu, packed)) { // queue the candidates, in start order (slice, lane, j)
+                uint32_t tot_packed;
+                const uint32_t ex = warp_exclusive(packed, lane, tot_packed);
+                uint32_t tot = 0;
+#pragma unroll
+                for (uint32_t sl = 0; sl < kSlices; ++sl) tot += (tot_packed >> (16 * sl)) & 0xFFFFu;
                 if (qn + tot > kQueue) { // warp-uniform
                     wk.flush(lo, qn);
                     qn = 0;
                 }
-                uint32_t at = qn + ex;
-                for (uint32_t m = mask; m; m &= m - 1)
-                    wk.q[at++] = uint16_t(g * kGroup + lane * kLaneStarts + __ffs(m) - 1);
+                uint32_t base = qn;
+#pragma unroll
+                for (uint32_t sl = 0; sl < kSlices; ++sl) {
+                    uint32_t at = base + ((ex >> (16 * sl)) & 0xFFFFu);
+                    const uint32_t first = g * kGroup + sl * kSliceSpan + lane * kSliceStarts;
+                    for (uint32_t m = mask[sl]; m; m &= m - 1) wk.q[at++] = uint16_t(first + __ffs(m) - 1);
+                    base += (tot_packed >> (16 * sl)) & 0xFFFFu;
+                }
                 qn += tot;
                 __syncwarp();
             }
@@ -595,9 +757,9 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
     const uint64_t c0 = min(nt, uint64_t(blockIdx.x) * chunk), c1 = min(nt, c0 + chunk);
     {
         uint32_t s = 0;
-        for (uint64_t i = c0 + tid; i < c1; i += kThreads) s += a.tile_count[i];
+        for (uint64_t i = c0 + tid; i < c1; i += NT) s += a.tile_count[i];
         uint32_t tot;
-        block_exclusive(s, s_scr, tot);
+        block_exclusive<NW>(s, s_scr, tot);
         if (tid == 0) a.chunk_sum[blockIdx.x] = tot;
     }
     grid.sync();
@@ -615,13 +777,13 @@ __global__ void __launch_bounds__(kThreads, 1) pfac_scan_kernel(const __grid_con
         *a.base_out = origin + total;
     }
     const bool fits = origin + total <= a.out_cap && *a.warp_need == 0;
-    for (uint64_t r0 = c0; r0 < c1; r0 += kThreads) {
+    for (uint64_t r0 = c0; r0 < c1; r0 += NT) {
         const uint64_t i = r0 + tid;
         const uint32_t n = i < c1 ? a.tile_count[i] : 0u;
         uint32_t tot;
-        const uint32_t ex = block_exclusive(n, s_scr, tot);
+        const uint32_t ex = block_exclusive<NW>(n, s_scr, tot);
         if (n && fits) {
-            const uint4* src = reinterpret_cast<const uint4*>(a.stage + (i % (uint64_t(gridDim.x) * kWarps)) * a.warp_cap) +
+            const uint4* src = reinterpret_cast<const uint4*>(a.stage + (i % (uint64_t(gridDim.x) * NW)) * a.warp_cap) +
                                a.tile_slot[i];
             uint4* dst = reinterpret_cast<uint4*>(a.out) + base + ex;
             for (uint32_t k = 0; k < n; ++k) dst[k] = src[k];
