@@ -293,9 +293,11 @@ struct Workspace {
     uint32_t* d_tile_ccount = nullptr;
     uint32_t* d_tile_cslot = nullptr;
     uint64_t ctile_cap = 0, ctile_cap2 = 0;
+    uint32_t* d_tile_region = nullptr;
+    uint64_t region_cap = 0;
     // [0] max records a warp needed (0 = fits), [1] total of the last launch,
     // [2] error word, [3] zero (base_in of a single launch), [4] its base_out,
-    // [5] max candidates a filter warp needed (0 = fits)
+    // [5] max candidates a filter warp needed (0 = fits), [6] dynamic unit counter
     unsigned long long* d_small = nullptr;
     unsigned long long* h_small = nullptr; // pinned mirror
     uint4* d_flush = nullptr;
@@ -321,7 +323,8 @@ struct Workspace {
         cudaStreamSynchronize(copy);
         for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
                         (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
-                        (void*)d_flush, (void*)d_cand, (void*)d_tile_ccount, (void*)d_tile_cslot})
+                        (void*)d_flush, (void*)d_cand, (void*)d_tile_ccount, (void*)d_tile_cslot,
+                        (void*)d_tile_region})
             cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
@@ -378,7 +381,7 @@ struct Workspace {
         regrow(d_tile_cslot, ctile_cap2, tiles);
     }
     // Clears the per-scan accumulators (overflow needs, error word).
-    void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 6 * sizeof(unsigned long long), stream)); }
+    void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 7 * sizeof(unsigned long long), stream)); }
 };
 
 std::mutex g_pool_mu;
@@ -501,6 +504,11 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         a.tile_cslot = ws.d_tile_cslot;
         a.cand_warps = uint32_t(fwarps);
         a.n_ftiles = l.n_ftiles;
+        ws.regrow(ws.d_tile_region, ws.region_cap, l.n_tiles);
+        a.tile_region = ws.d_tile_region;
+        a.unit_next = ws.d_small + 6;
+        // streamed chunks share the counter: zero it before each launch
+        CK(cudaMemsetAsync(ws.d_small + 6, 0, sizeof(unsigned long long), ws.stream));
     }
     void* params[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(l.grid)),

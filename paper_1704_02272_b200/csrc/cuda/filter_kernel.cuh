@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             if (lane == 31 && sbase + kFStep < avail16)
                 tail = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
 
+            const bool full = (s + 1) * kFStep <= rem; // warp-uniform: every start of the step may report
             uint32_t mask[kFChunks];
             uint32_t packed_lo = 0, packed_hi = 0; // survivor counts, 16 bits per chunk
 #pragma unroll
@@ -145,9 +146,11 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                 *reinterpret_cast<uint4*>(stage + b * kFStageStride + 16u * lane) = cur[b];
                 if (lane == 31) *reinterpret_cast<uint32_t*>(stage + b * kFStageStride + kFChunk) = ov;
                 const uint32_t w[5] = {cur[b].x, cur[b].y, cur[b].z, cur[b].w, ov};
-                const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
-                const uint32_t valid = r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
-                mask[b] = f_pair_level1(w, tbase, shift) & valid;
+                mask[b] = f_pair_level1(w, tbase, shift);
+                if (!full) {
+                    const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
+                    mask[b] &= r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+                }
                 const uint32_t c = uint32_t(__popc(mask[b]));
                 if (b < 2) packed_lo |= c << (16 * b);
                 else packed_hi |= c << (16 * (b - 2));

@@ -93,6 +93,8 @@ struct ScanArgs {
     const uint32_t* tile_cslot;
     uint32_t cand_warps;        // tile t's candidates live in region t % cand_warps
     uint64_t n_ftiles;          // filter tiles; n_tiles then counts walk units of kSuper tiles
+    unsigned long long* unit_next; // dynamic unit counter (zero at launch)
+    uint32_t* tile_region;      // staging region (warp) of each unit
 };
 
 // ---- text and dictionary helpers --------------------------------------------------
@@ -164,11 +166,26 @@ struct Sink {
 };
 
 // text[start, start + len) == the pattern stored at byte offset `off`.
+// 32 bytes per block with every load of the block issued before the first
+// compare (one memory latency per block instead of one per word).
 __device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint64_t off, uint32_t len)
 {
     const uint32_t* p = reinterpret_cast<const uint32_t*>(a.trie.pat_bytes + off);
-    for (uint32_t i = 0; i < len; i += 4)
-        if ((text_word(a, start + i) ^ __ldg(p + i / 4)) & tail_mask(len - i)) return false;
+    const uint32_t sh = uint32_t(start & 3u) * 8u;
+    for (uint32_t i = 0; i < len; i += 32) {
+        const uint32_t* tw = reinterpret_cast<const uint32_t*>(a.text + ((start + i) & ~3ull));
+        const uint32_t nw = min(8u, (len - i + 3) / 4); // pattern words in this block
+        uint32_t t[9], pw[8];
+#pragma unroll
+        for (uint32_t k = 0; k < 9; ++k) t[k] = k <= nw ? __ldg(tw + k) : 0u; // padded text: safe to overread
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) pw[k] = k < nw ? __ldg(p + i / 4 + k) : 0u;
+        uint32_t diff = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+            if (k < nw) diff |= ((sh ? __funnelshift_r(t[k], t[k + 1], sh) : t[k]) ^ pw[k]) & tail_mask(len - i - 4 * k);
+        if (diff) return false;
+    }
     return true;
 }
 
@@ -627,38 +644,79 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
         // Walk units of kSuper filter tiles: lane i < kSuper fetches tile i's
         // candidate count and slot, so one load latency covers the unit, and
         // rounds are filled across tile boundaries.
-        for (uint64_t unit = gw; unit < a.n_tiles; unit += W) {
+        // Units are handed out dynamically (warps finish unevenly: walks
+        // are latency chains); the unit records which region staged it.
+        for (;;) {
+            uint64_t unit = 0;
+            if (lane == 0) unit = atomicAdd(a.unit_next, 1ull);
+            unit = __shfl_sync(0xFFFFFFFFu, unit, 0);
+            if (unit >= a.n_tiles) break;
             const uint64_t lo = unit * uint64_t(kSuper) * kTile;
             const uint64_t slot = wk.cursor;
             const uint64_t ft = unit * kSuper + lane;
             uint32_t cnt = 0, cslot = 0;
             if (lane < kSuper && ft < a.n_ftiles) cnt = a.tile_ccount[ft], cslot = a.tile_cslot[ft];
-            uint32_t qn = 0;
-            for (uint32_t i = 0; i < kSuper; ++i) {
-                const uint32_t n_i = __shfl_sync(0xFFFFFFFFu, cnt, i);
-                if (n_i == 0) continue;
-                const uint32_t s_i = __shfl_sync(0xFFFFFFFFu, cslot, i);
-                const uint64_t t_i = unit * kSuper + i;
-                const uint16_t* src = a.cand + (t_i % a.cand_warps) * a.cand_cap + s_i;
-                for (uint32_t c0 = 0; c0 < n_i;) {
-                    if (qn == kQueue) {
-                        __syncwarp();
-                        wk.flush(lo, qn);
-                        qn = 0;
-                    }
-                    const uint32_t n = min(kQueue - qn, n_i - c0);
-                    for (uint32_t k = lane; k < n; k += 32) wk.q[qn + k] = uint16_t(src[c0 + k] + i * kTile);
-                    qn += n;
-                    c0 += n;
-                }
+            uint32_t pre = cnt; // inclusive prefix over lanes 0..kSuper-1
+#pragma unroll
+            for (uint32_t d = 1; d < kSuper; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += u;
             }
-            if (qn) {
-                __syncwarp();
-                wk.flush(lo, qn);
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, pre, kSuper - 1);
+            pre -= cnt; // exclusive
+            if (total <= kQueue) {
+                // every entry of the unit loaded at once: entry f belongs to
+                // the last tile i with pre_i <= f
+                uint32_t pres[kSuper], slots[kSuper];
+#pragma unroll
+                for (uint32_t i = 0; i < kSuper; ++i) {
+                    pres[i] = __shfl_sync(0xFFFFFFFFu, pre, i);
+                    slots[i] = __shfl_sync(0xFFFFFFFFu, cslot, i);
+                }
+                for (uint32_t f = lane; f < total; f += 32) {
+                    uint32_t i = 0;
+#pragma unroll
+                    for (uint32_t k = 1; k < kSuper; ++k) i += f >= pres[k] ? 1u : 0u;
+                    uint32_t p_i = pres[0], s_i = slots[0];
+#pragma unroll
+                    for (uint32_t k = 1; k < kSuper; ++k)
+                        if (i == k) p_i = pres[k], s_i = slots[k];
+                    const uint64_t t_i = unit * kSuper + i;
+                    wk.q[f] = uint16_t(a.cand[(t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i)] + i * kTile);
+                }
+                if (total) {
+                    __syncwarp();
+                    wk.flush(lo, total);
+                }
+            } else {
+                uint32_t qn = 0;
+                for (uint32_t i = 0; i < kSuper; ++i) {
+                    const uint32_t n_i = __shfl_sync(0xFFFFFFFFu, cnt, i);
+                    if (n_i == 0) continue;
+                    const uint32_t s_i = __shfl_sync(0xFFFFFFFFu, cslot, i);
+                    const uint64_t t_i = unit * kSuper + i;
+                    const uint16_t* src = a.cand + (t_i % a.cand_warps) * a.cand_cap + s_i;
+                    for (uint32_t c0 = 0; c0 < n_i;) {
+                        if (qn == kQueue) {
+                            __syncwarp();
+                            wk.flush(lo, qn);
+                            qn = 0;
+                        }
+                        const uint32_t n = min(kQueue - qn, n_i - c0);
+                        for (uint32_t k = lane; k < n; k += 32) wk.q[qn + k] = uint16_t(src[c0 + k] + i * kTile);
+                        qn += n;
+                        c0 += n;
+                    }
+                }
+                if (qn) {
+                    __syncwarp();
+                    wk.flush(lo, qn);
+                }
             }
             if (lane == 0) {
                 a.tile_count[unit] = uint32_t(wk.cursor - slot);
                 a.tile_slot[unit] = uint32_t(slot);
+                a.tile_region[unit] = gw;
             }
         }
     }
@@ -783,8 +841,8 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
         uint32_t tot;
         const uint32_t ex = block_exclusive<NW>(n, s_scr, tot);
         if (n && fits) {
-            const uint4* src = reinterpret_cast<const uint4*>(a.stage + (i % (uint64_t(gridDim.x) * NW)) * a.warp_cap) +
-                               a.tile_slot[i];
+            const uint64_t region = CANDS ? a.tile_region[i] : i % (uint64_t(gridDim.x) * NW);
+            const uint4* src = reinterpret_cast<const uint4*>(a.stage + region * a.warp_cap) + a.tile_slot[i];
             uint4* dst = reinterpret_cast<uint4*>(a.out) + base + ex;
             for (uint32_t k = 0; k < n; ++k) dst[k] = src[k];
         }
