@@ -223,6 +223,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.mul_shr8 = 1u << 24;
     v.mul_shr16 = 1u << 16;
     v.filter2 = d->upload(im.filter2);
+    v.key4 = d->upload(im.key4.empty() ? std::vector<uint32_t>(1, 0u) : im.key4);
+    v.key4_words = uint32_t(im.key4.size());
     v.filter2_bits = im.filter2_bits;
     v.jump = d->upload(im.jump);
     v.jump_bits = im.jump_bits;
@@ -231,7 +233,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     d->pair = im.filter_mode == 2 && pair_pipeline_enabled();
     if (d->pair) {
         d->kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
-        d->smem = gpu::smem_fixed_bytes(true); // no filter table in the walking pass
+        d->smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
         d->warps = gpu::kCWarps;
         d->filter_smem = size_t(v.filter_words) * 4 + gpu::filter_smem_fixed_bytes();
         CK(cudaFuncSetAttribute(gpu::pfac_pair_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -289,7 +291,8 @@ struct Workspace {
     unsigned long long* d_bases = nullptr; // streamed: records before chunk c
     uint64_t bases_cap = 0;
     uint16_t* d_cand = nullptr;            // pair pipeline: per filter warp candidate regions
-    uint64_t cand_alloc = 0, cand_cap = 0;
+    uint32_t* d_cand_key = nullptr;        // their first 4 text bytes
+    uint64_t cand_alloc = 0, cand_cap = 0, key_alloc = 0;
     uint32_t* d_tile_ccount = nullptr;
     uint32_t* d_tile_cslot = nullptr;
     uint64_t ctile_cap = 0, ctile_cap2 = 0;
@@ -323,7 +326,7 @@ struct Workspace {
         cudaStreamSynchronize(copy);
         for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
                         (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
-                        (void*)d_flush, (void*)d_cand, (void*)d_tile_ccount, (void*)d_tile_cslot,
+                        (void*)d_flush, (void*)d_cand, (void*)d_cand_key, (void*)d_tile_ccount, (void*)d_tile_cslot,
                         (void*)d_tile_region})
             cudaFree(p);
         cudaFreeHost(h_small);
@@ -374,6 +377,7 @@ struct Workspace {
     {
         cand_cap = std::max(cand_cap, per_warp);
         regrow(d_cand, cand_alloc, warps * cand_cap);
+        regrow(d_cand_key, key_alloc, warps * cand_cap);
     }
     void ensure_ctiles(uint64_t tiles)
     {
@@ -492,6 +496,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.start_end = n_avail >= me ? std::min(n_own, n_avail - me + 1) : 0;
         f.n_tiles = l.n_ftiles;
         f.cand = ws.d_cand;
+        f.cand_key = ws.d_cand_key;
         f.cand_cap = ws.cand_cap;
         f.tile_ccount = ws.d_tile_ccount;
         f.tile_cslot = ws.d_tile_cslot;
@@ -499,6 +504,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         gpu::pfac_pair_filter_kernel<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());
         a.cand = ws.d_cand;
+        a.cand_key = ws.d_cand_key;
         a.cand_cap = ws.cand_cap;
         a.tile_ccount = ws.d_tile_ccount;
         a.tile_cslot = ws.d_tile_cslot;

@@ -53,6 +53,7 @@ struct FilterArgs {
     uint64_t start_end;      // starts [0, start_end) may report
     uint64_t n_tiles;
     uint16_t* cand;          // gridDim.x * kFWarps regions of cand_cap entries
+    uint32_t* cand_key;      // same layout: the survivor's first 4 text bytes
     uint64_t cand_cap;
     uint32_t* tile_ccount;
     uint32_t* tile_cslot;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                 __syncwarp();
                 for (uint32_t r0 = 0; r0 < base; r0 += 32) {
                     const uint32_t e = r0 + lane;
-                    uint32_t off = 0;
+                    uint32_t off = 0, y = 0;
                     bool keep = false;
                     if (e < base) {
                         off = q[e]; // tile-relative start
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                         uint32_t lo4, hi4;
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo4) : "r"(sa & ~3u));
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi4) : "r"((sa & ~3u) + 4));
-                        const uint32_t y = __funnelshift_r(lo4, hi4, 8 * (sa & 3u)); // bytes off..off+3
+                        y = __funnelshift_r(lo4, hi4, 8 * (sa & 3u)); // bytes off..off+3
                         const bool odd = off & 1u;
                         const uint32_t mid = odd ? (y >> 8) : y;
                         const uint32_t amt = odd ? y : (y >> 24);
@@ -207,7 +208,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
                     if (keep) {
                         const uint64_t at = cursor + __popc(bal & below);
-                        if (at < a.cand_cap) region[at] = uint16_t(off);
+                        if (at < a.cand_cap) {
+                            region[at] = uint16_t(off);
+                            a.cand_key[uint64_t(gw) * a.cand_cap + at] = y;
+                        }
                     }
                     cursor += __popc(bal);
                 }

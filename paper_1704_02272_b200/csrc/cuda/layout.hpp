@@ -124,6 +124,8 @@ struct TrieView {
     uint32_t mul_shr16;   // IMAD.HI, balancing the filter's ALU (shift) and FMA pipes
     const uint32_t* filter2; // second level, 2^filter2_bits bits
     uint32_t filter2_bits;   // 0 = no second level
+    const uint32_t* key4;    // pair pipeline: bitmap over the first 4 bytes of every depth-k path
+    uint32_t key4_words;     // (single-probe hash, layout above); 0 = none
     const uint32_t* jump;    // 2^jump_bits uint4 slots
     uint32_t jump_bits;      // 0 = no jump table (walks start at the root)
     uint32_t min_emit;

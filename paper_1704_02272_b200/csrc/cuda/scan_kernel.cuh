@@ -88,6 +88,7 @@ struct ScanArgs {
     unsigned int* err;
     // CANDS launches: per-tile start candidates from pfac_pair_filter_kernel
     const uint16_t* cand;       // cand_warps regions of cand_cap tile-relative offsets
+    const uint32_t* cand_key;   // their first 4 text bytes
     uint64_t cand_cap;
     const uint32_t* tile_ccount;
     const uint32_t* tile_cslot;
@@ -596,7 +597,8 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
 {
     constexpr uint32_t NW = CANDS ? kCWarps : kWarps, NT = NW * 32;
     extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t fwords = (KW && !CANDS) ? a.trie.filter_words : 0u;
+    // first in shared memory: the start filter (fused) or the 4-byte-prefix bitmap (CANDS)
+    const uint32_t fwords = CANDS ? a.trie.key4_words : (KW ? a.trie.filter_words : 0u);
     uint32_t* s_filter = reinterpret_cast<uint32_t*>(smem);                   // first: 2^bits / 8 bytes
     uint8_t* s_ring = smem + size_t(fwords) * 4;                               // [warp][stage][kStageBytes]
     uint16_t* s_queue = reinterpret_cast<uint16_t*>(s_ring + (CANDS ? 0u : NW * kStages * kStageBytes));
@@ -606,7 +608,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const TrieView& t = a.trie;
-    for (uint32_t i = tid; i < fwords; i += NT) s_filter[i] = __ldg(t.filter + i);
+    for (uint32_t i = tid; i < fwords; i += NT) s_filter[i] = __ldg((CANDS ? t.key4 : t.filter) + i);
     if (!IDENT)
         for (uint32_t i = tid; i < 256; i += NT) s_sym[i] = __ldg(t.symtab + i);
 
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                 const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, pre, d);
                 if (lane >= d) pre += u;
             }
-            const uint32_t total = __shfl_sync(0xFFFFFFFFu, pre, kSuper - 1);
+            uint32_t total = __shfl_sync(0xFFFFFFFFu, pre, kSuper - 1);
             pre -= cnt; // exclusive
             if (total <= kQueue) {
                 // every entry of the unit loaded at once: entry f belongs to
@@ -673,17 +675,38 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                     pres[i] = __shfl_sync(0xFFFFFFFFu, pre, i);
                     slots[i] = __shfl_sync(0xFFFFFFFFu, cslot, i);
                 }
-                for (uint32_t f = lane; f < total; f += 32) {
-                    uint32_t i = 0;
+                // Entries are re-checked against the 4-byte-prefix bitmap
+                // (one shared-memory probe) and compacted in order: most
+                // pair survivors are false positives, and each would cost
+                // an L2 round trip in the walk.
+                const uint32_t kmask4 = (fwords - 1u) << 2;
+                const uint8_t* kbytes = reinterpret_cast<const uint8_t*>(s_filter);
+                uint32_t kept = 0;
+                for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+                    const uint32_t f = f0 + lane;
+                    bool keep = false;
+                    uint16_t v = 0;
+                    if (f < total) {
+                        uint32_t i = 0;
 #pragma unroll
-                    for (uint32_t k = 1; k < kSuper; ++k) i += f >= pres[k] ? 1u : 0u;
-                    uint32_t p_i = pres[0], s_i = slots[0];
+                        for (uint32_t k = 1; k < kSuper; ++k) i += f >= pres[k] ? 1u : 0u;
+                        uint32_t p_i = pres[0], s_i = slots[0];
 #pragma unroll
-                    for (uint32_t k = 1; k < kSuper; ++k)
-                        if (i == k) p_i = pres[k], s_i = slots[k];
-                    const uint64_t t_i = unit * kSuper + i;
-                    wk.q[f] = uint16_t(a.cand[(t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i)] + i * kTile);
+                        for (uint32_t k = 1; k < kSuper; ++k)
+                            if (i == k) p_i = pres[k], s_i = slots[k];
+                        const uint64_t t_i = unit * kSuper + i;
+                        const uint64_t at = (t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i);
+                        v = uint16_t(a.cand[at] + i * kTile);
+                        const uint32_t key = a.cand_key[at];
+                        const uint32_t word =
+                            *reinterpret_cast<const uint32_t*>(kbytes + (__umulhi(key, kFilterMul) & kmask4));
+                        keep = fwords == 0 || int32_t(word << (key & 31u)) < 0;
+                    }
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                    if (keep) wk.q[kept + __popc(bal & ((1u << lane) - 1u))] = v;
+                    kept += __popc(bal);
                 }
+                total = kept;
                 if (total) {
                     __syncwarp();
                     wk.flush(lo, total);

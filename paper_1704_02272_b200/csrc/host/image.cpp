@@ -28,7 +28,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + jump.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -369,6 +369,13 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             if (opt.filter_mode == 1) use_pair = false;
             if (opt.filter_mode == 2) use_pair = k >= 4;
             if (use_pair) {
+                // the walking pass re-checks survivors' first 4 bytes in shared memory
+                const uint32_t kb = std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, 20);
+                im.key4.assign((size_t(1) << kb) / 32, 0u);
+                for (uint64_t g : grams) {
+                    const uint32_t k32 = uint32_t(g);
+                    im.key4[filter_word(k32, kb - 5)] |= filter_mask_bit(k32);
+                }
                 im.filter_mode = 2;
                 im.filter = std::move(pair);
                 im.filter_bits = pair_wb + 5;
