@@ -59,6 +59,12 @@ hepfac_status_t hepfac_b200_session_create(const hepfac_trie_t* trie, const uint
  * flush_l2 != 0 evicts L2 before each (untimed). */
 hepfac_status_t hepfac_b200_session_run(hepfac_b200_session_t* session, uint32_t iterations,
                                         int flush_l2, double* ms_each, uint64_t* matches);
+/* Per-kernel device times of the last run's scans (CUDA events on the
+ * engine's stream): first = the filter pass of the pair pipeline, or the fused
+ * scan kernel; second = the candidate-walking pass (0 when there is none).
+ * *kernels_per_scan (may be NULL) = kernel launches per scan (1 or 2). */
+hepfac_status_t hepfac_b200_session_kernel_ms(hepfac_b200_session_t* session, uint32_t iterations,
+                                              double* first_ms, double* second_ms, uint32_t* kernels_per_scan);
 /* Copies the last run's sorted matches to the host. */
 hepfac_status_t hepfac_b200_session_fetch(hepfac_b200_session_t* session,
                                           hepfac_match_list_t** out);

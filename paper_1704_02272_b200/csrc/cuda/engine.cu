@@ -448,7 +448,7 @@ Launch plan(const DeviceTrie& dt, uint64_t n_own)
 // stores *base_in + total to *base_out.
 uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text, uint64_t n_own,
                       uint64_t n_avail, uint64_t g0, const unsigned long long* base_in = nullptr,
-                      unsigned long long* base_out = nullptr)
+                      unsigned long long* base_out = nullptr, cudaEvent_t between = nullptr)
 {
     const Launch l = plan(dt, n_own);
     if (!base_in) base_in = ws.d_small + 3, base_out = ws.d_small + 4;
@@ -503,6 +503,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.cand_need = ws.d_small + 5;
         gpu::pfac_pair_filter_kernel<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());
+        if (between) CK(cudaEventRecord(between, ws.stream));
         a.cand = ws.d_cand;
         a.cand_key = ws.d_cand_key;
         a.cand_cap = ws.cand_cap;
@@ -774,7 +775,8 @@ struct Session {
     std::shared_ptr<DeviceTrie> dt;
     std::unique_ptr<Workspace> ws;
     uint64_t bytes = 0, matches = 0, offset = 0, owned = 0;
-    bool complete = false;
+    bool complete = false, split = false;
+    uint32_t last_iterations = 0;
     std::vector<cudaEvent_t> evs;
     ~Session()
     {
@@ -813,7 +815,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         ws.flush_n16 = size_t(l2) * 2 / 16;
         ws.d_flush = dev_alloc<uint4>(ws.flush_n16);
     }
-    while (s->evs.size() < 2 * size_t(iterations)) {
+    while (s->evs.size() < 3 * size_t(iterations)) {
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
         s->evs.push_back(e);
@@ -822,14 +824,29 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
     for (uint32_t i = 0; i < iterations; ++i) {
         if (flush_l2)
             gpu::l2_flush_kernel<<<dt.sm_count * 4, 512, 0, ws.stream>>>(ws.d_flush, ws.flush_n16, i);
-        CK(cudaEventRecord(s->evs[2 * i], ws.stream));
-        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset);
-        CK(cudaEventRecord(s->evs[2 * i + 1], ws.stream));
+        CK(cudaEventRecord(s->evs[3 * i], ws.stream));
+        if (can_match) enqueue_scan(dt, ws, ws.d_text, s->owned, s->bytes, s->offset, nullptr, nullptr, s->evs[3 * i + 1]);
+        CK(cudaEventRecord(s->evs[3 * i + 2], ws.stream));
     }
+    s->last_iterations = iterations;
+    s->split = can_match && dt.pair;
     s->complete = !can_match || fetch_small(ws, dt, s->owned); // grows buffers for the next run
     s->matches = can_match ? records_of(ws) : 0;
     for (uint32_t i = 0; i < iterations; ++i)
-        if (ms_each) ms_each[i] = elapsed_ms(s->evs[2 * i], s->evs[2 * i + 1]);
+        if (ms_each) ms_each[i] = elapsed_ms(s->evs[3 * i], s->evs[3 * i + 2]);
+}
+
+void session_split(Session* s, uint32_t n, double* first_ms, double* second_ms, uint32_t* kernels_per_scan)
+{
+    DeviceGuard g(s->ws->device);
+    if (kernels_per_scan) *kernels_per_scan = s->dt->pair ? 2u : 1u;
+    n = std::min(n, s->last_iterations);
+    for (uint32_t i = 0; i < n; ++i) {
+        const double total = elapsed_ms(s->evs[3 * i], s->evs[3 * i + 2]);
+        const double first = s->split ? elapsed_ms(s->evs[3 * i], s->evs[3 * i + 1]) : total;
+        if (first_ms) first_ms[i] = first;
+        if (second_ms) second_ms[i] = total - first;
+    }
 }
 
 uint64_t session_matches(Session* s) { return s->matches; }

@@ -58,6 +58,9 @@ struct Session;
 Session* session_create(const Trie& t, const uint8_t* host_text, uint64_t bytes, uint64_t offset, uint64_t owned);
 void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each);
 uint64_t session_matches(Session* s);
+// Per-kernel device times of the last run: first = filter pass (or the fused
+// scan kernel), second = candidate-walking pass (0 without the pair pipeline).
+void session_split(Session* s, uint32_t n, double* first_ms, double* second_ms, uint32_t* kernels_per_scan);
 std::unique_ptr<MatchList> session_fetch(Session* s);
 void session_destroy(Session* s);
 

@@ -160,6 +160,8 @@ _B200_PROTOTYPES = [
     ("hepfac_b200_scan_shard", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.c_uint64, _PP]),
     ("hepfac_b200_last_scan_stats", C.c_int, [C.POINTER(_ScanStats)]),
     ("hepfac_b200_session_create", C.c_int, [_P, _P, C.c_uint64, C.c_uint64, C.c_uint64, _PP]),
+    ("hepfac_b200_session_kernel_ms", C.c_int, [_P, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                C.POINTER(C.c_uint32)]),
     ("hepfac_b200_session_run", C.c_int, [_P, C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                           C.POINTER(C.c_uint64)]),
     ("hepfac_b200_session_fetch", C.c_int, [_P, _PP]),
@@ -494,6 +496,14 @@ class Session:
         m = C.c_uint64()
         self.lib.check(self.lib.dll.hepfac_b200_session_run(self.h, iterations, int(flush_l2), ms, C.byref(m)))
         return list(ms)[:iterations], m.value
+
+    def kernel_ms(self, iterations: int):
+        """Per-kernel device ms of the last run: (first pass, second pass, kernels per scan)."""
+        a = (C.c_double * max(1, iterations))()
+        b = (C.c_double * max(1, iterations))()
+        k = C.c_uint32()
+        self.lib.check(self.lib.dll.hepfac_b200_session_kernel_ms(self.h, iterations, a, b, C.byref(k)))
+        return list(a)[:iterations], list(b)[:iterations], k.value
 
     def fetch(self) -> np.ndarray:
         h = C.c_void_p()
