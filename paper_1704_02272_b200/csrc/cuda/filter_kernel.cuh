@@ -102,8 +102,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
     const uint32_t shift = a.pair_shift;
     const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
     uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
+    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
     uint64_t cursor = 0;
     const uint32_t below = (1u << lane) - 1u;
+    static_assert(kFChunks * kFStageStride <= 2112, "staging offset -> chunk division assumes 4 chunks of 528 B");
 
     // 16 bytes of lane `lane` of chunk at text offset `at` (zeros past the buffer)
     auto load = [&](uint64_t at) -> uint4 {
@@ -140,9 +142,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             uint32_t packed_lo = 0, packed_hi = 0; // survivor counts, 16 bits per chunk
 #pragma unroll
             for (uint32_t b = 0; b < kFChunks; ++b) {
-                const uint32_t from_next = __shfl_sync(0xFFFFFFFFu, cur[(b + 1) % kFChunks].x, 0);
-                uint32_t ov = __shfl_sync(0xFFFFFFFFu, cur[b].x, (lane + 1) & 31u);
-                if (lane == 31) ov = b + 1 < kFChunks ? from_next : tail;
+                // lane 0 sends the next chunk's first word (lane 31 reads it)
+                const uint32_t send = (lane == 0 && b + 1 < kFChunks) ? cur[(b + 1) % kFChunks].x : cur[b].x;
+                uint32_t ov = __shfl_sync(0xFFFFFFFFu, send, (lane + 1) & 31u);
+                if (lane == 31 && b + 1 == kFChunks) ov = tail;
                 // stage the slice for the second level
                 *reinterpret_cast<uint4*>(stage + b * kFStageStride + 16u * lane) = cur[b];
                 if (lane == 31) *reinterpret_cast<uint32_t*>(stage + b * kFStageStride + kFChunk) = ov;
@@ -177,29 +180,36 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             // Queue chunks [b0, b1) (their candidates fit), then test them in
             // full rounds and append the survivors to the region.
             auto run = [&](uint32_t b0, uint32_t b1) {
+                // Queue entries are staging offsets (chunk * 528 + 16 * lane + j),
+                // written two per iteration: lowest bit forward, highest bit
+                // backward.
                 uint32_t base = 0;
 #pragma unroll
                 for (uint32_t b = 0; b < kFChunks; ++b) {
                     if (b < b0 || b >= b1) continue;
-                    uint32_t at = base + ex[b];
-                    const uint32_t first = s * kFStep + b * kFChunk + 16u * lane;
-                    for (uint32_t m = mask[b]; m; m &= m - 1) q[at++] = uint16_t(first + __ffs(m) - 1);
+                    uint32_t at = base + ex[b], back = at + __popc(mask[b]) - 1;
+                    const uint32_t first = b * kFStageStride + 16u * lane;
+                    for (uint32_t m = mask[b]; m;) {
+                        const uint32_t lo = __ffs(m) - 1, hi = 31 - __clz(m);
+                        q[at++] = uint16_t(first + lo);
+                        if (hi != lo) q[back--] = uint16_t(first + hi);
+                        m &= ~((1u << lo) | (1u << hi));
+                    }
                     base += tot[b];
                 }
                 __syncwarp();
                 for (uint32_t r0 = 0; r0 < base; r0 += 32) {
                     const uint32_t e = r0 + lane;
-                    uint32_t off = 0, y = 0;
+                    uint32_t so = 0, y = 0;
                     bool keep = false;
                     if (e < base) {
-                        off = q[e]; // tile-relative start
-                        const uint32_t in_step = off - s * kFStep;
-                        const uint32_t sa = stage_s + (in_step >> 9) * kFStageStride + (in_step & (kFChunk - 1));
+                        so = q[e]; // staging offset of the start
+                        const uint32_t sa = stage_s + so;
                         uint32_t lo4, hi4;
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo4) : "r"(sa & ~3u));
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi4) : "r"((sa & ~3u) + 4));
                         y = __funnelshift_r(lo4, hi4, 8 * (sa & 3u)); // bytes off..off+3
-                        const bool odd = off & 1u;
+                        const bool odd = so & 1u; // chunk and lane offsets are even
                         const uint32_t mid = odd ? (y >> 8) : y;
                         const uint32_t amt = odd ? y : (y >> 24);
                         const uint32_t word = f_lds(tbase + (((mid * kPairMul) >> shift) << 2));
@@ -209,8 +219,9 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                     if (keep) {
                         const uint64_t at = cursor + __popc(bal & below);
                         if (at < a.cand_cap) {
-                            region[at] = uint16_t(off);
-                            a.cand_key[uint64_t(gw) * a.cand_cap + at] = y;
+                            const uint32_t c = (so * 125u) >> 16; // so / 528 for every valid so < 2112
+                            region[at] = uint16_t(s * kFStep + so - 16u * c);
+                            keys[at] = y;
                         }
                     }
                     cursor += __popc(bal);
