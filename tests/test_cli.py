@@ -74,7 +74,9 @@ def test_cli_match_equals_reference(tmp_path, gpu, ref, depth):
     pf, tf, inp = tmp_path / "p.txt", tmp_path / "t.htri", tmp_path / "in.bin"
     write_patterns(pf, pats)
     inp.write_bytes(t.tobytes())
-    assert run("build", "--patterns", str(pf), "--sigma", "256", "--compress", "2", "--out", str(tf)).returncode == 0
+    # the benchmark trie for --depth is stage 1 (a tail-merged trie cannot be truncated)
+    stages = "1" if depth else "2"
+    assert run("build", "--patterns", str(pf), "--sigma", "256", "--compress", stages, "--out", str(tf)).returncode == 0
     args = ["match", "--trie", str(tf), "--input", str(inp)] + (["--depth", str(depth)] if depth else [])
     r = run(*args)
     assert r.returncode == 0, r.stderr
@@ -89,3 +91,13 @@ def test_cli_match_equals_reference(tmp_path, gpu, ref, depth):
     out = tmp_path / "m.txt"
     assert run(*args, "--out", str(out)).returncode == 0
     assert out.read_bytes() == r.stdout
+
+
+@pytest.mark.gpu
+def test_cli_match_truncate_stage2_is_invalid(tmp_path, gpu):
+    pf, tf, inp = tmp_path / "p.txt", tmp_path / "t.htri", tmp_path / "in.bin"
+    write_patterns(pf, [b"abcd", b"abce", b"xbcd"])
+    inp.write_bytes(b"zzabcdzz")
+    assert run("build", "--patterns", str(pf), "--compress", "2", "--out", str(tf)).returncode == 0
+    r = run("match", "--trie", str(tf), "--input", str(inp), "--depth", "2")
+    assert r.returncode == 1 and b"truncate" in r.stderr
