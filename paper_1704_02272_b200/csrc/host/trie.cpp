@@ -15,12 +15,71 @@
 // level from the symbol-sorted pattern list (no pointer graph, no queue),
 // and rewrites operate on a flat CSR graph.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
+#include <thread>
 #include <unordered_map>
 
 #include "core.hpp"
 
 namespace hfb {
+
+namespace {
+
+// Host compiler threads: HEPFAC_COMPILER_THREADS, else the hardware threads.
+unsigned compiler_threads()
+{
+    if (const char* s = std::getenv("HEPFAC_COMPILER_THREADS")) {
+        const long v = std::strtol(s, nullptr, 10);
+        if (v >= 1 && v <= 1024) return unsigned(v);
+    }
+    return std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+}
+
+// fn(begin, end) over [0, n) in contiguous slices, one per thread; serial
+// below `grain` items.  Results must not depend on the slicing.
+template <typename Fn>
+void parallel_slices(size_t n, size_t grain, Fn&& fn)
+{
+    const unsigned t = unsigned(std::min<size_t>(compiler_threads(), std::max<size_t>(1, n / std::max<size_t>(grain, 1))));
+    if (t <= 1) {
+        fn(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(t);
+    for (unsigned i = 0; i < t; ++i)
+        pool.emplace_back([&, i] { fn(n * i / t, n * (i + 1) / t); });
+    for (auto& th : pool) th.join();
+}
+
+// Stable order of `v` under `less`, sorted in parallel slices and merged
+// pairwise (the result equals std::stable_sort's).
+template <typename T, typename Less>
+void parallel_sort(std::vector<T>& v, Less less)
+{
+    const size_t n = v.size();
+    const unsigned t = unsigned(std::min<size_t>(compiler_threads(), std::max<size_t>(1, n / 65536)));
+    if (t <= 1) {
+        std::stable_sort(v.begin(), v.end(), less);
+        return;
+    }
+    std::vector<size_t> cut(t + 1);
+    for (unsigned i = 0; i <= t; ++i) cut[i] = n * i / t;
+    parallel_slices(t, 1, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) std::stable_sort(v.begin() + cut[i], v.begin() + cut[i + 1], less);
+    });
+    for (size_t width = 1; width < t; width *= 2) {
+        std::vector<std::thread> pool;
+        for (size_t i = 0; i + width < t; i += 2 * width) {
+            const size_t lo = cut[i], mid = cut[i + width], hi = cut[std::min<size_t>(t, i + 2 * width)];
+            pool.emplace_back([&, lo, mid, hi] { std::inplace_merge(v.begin() + lo, v.begin() + mid, v.begin() + hi, less); });
+        }
+        for (auto& th : pool) th.join();
+    }
+}
+
+} // namespace
 
 std::string format_mib(uint64_t bytes)
 {
@@ -80,14 +139,17 @@ std::unique_ptr<Trie> build_trie(const PatternSet& set)
     const Alphabet& a = set.alphabet;
     const size_t n = set.patterns.size();
     std::vector<std::string> keys(n); // symbol-index strings: byte order == symbol order
-    for (size_t i = 0; i < n; ++i) {
-        const std::string& p = set.patterns[i];
-        keys[i].resize(p.size());
-        for (size_t j = 0; j < p.size(); ++j) keys[i][j] = char(a.symbol_of(uint8_t(p[j])));
-    }
+    parallel_slices(n, 16384, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            const std::string& p = set.patterns[i];
+            keys[i].resize(p.size());
+            for (size_t j = 0; j < p.size(); ++j) keys[i][j] = char(a.symbol_of(uint8_t(p[j])));
+        }
+    });
     std::vector<uint32_t> order(n);
     std::iota(order.begin(), order.end(), 0u);
-    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return keys[x] < keys[y]; });
+    // patterns are distinct, so any sort gives the same order
+    parallel_sort(order, [&](uint32_t x, uint32_t y) { return keys[x] < keys[y]; });
 
     auto t = std::make_unique<Trie>(a);
     const uint32_t stride = t->stride();
@@ -292,10 +354,10 @@ std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
     Graph g = graph_of(t);
     const Alphabet& a = t.alphabet;
 
-    auto child_by_sym = [&](uint32_t u, uint32_t s) {
-        for (uint32_t e = g.first[u]; e < g.first[u] + g.degree[u]; ++e)
-            if (g.sym[e] == s) return g.dst[e];
-        return Trie::kNone;
+    auto child_by_sym = [&](uint32_t u, uint32_t s) { // edges are symbol-ascending
+        const auto b = g.sym.begin() + g.first[u], e = b + g.degree[u];
+        const auto it = std::lower_bound(b, e, uint16_t(s));
+        return (it != e && *it == s) ? g.dst[size_t(it - g.sym.begin())] : Trie::kNone;
     };
     auto leaf_terminal = [&](uint32_t u) { return g.term[u] && g.degree[u] == 0; };
     // A suffix of k <= 3 raw bytes, tagged with k, packed into 32 bits.
@@ -308,44 +370,69 @@ std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
     std::unordered_map<uint32_t, uint32_t> rep_of_suffix; // suffix -> representative node
     std::vector<std::pair<uint32_t, uint32_t>> reps;      // (node, suffix) in creation order
     std::vector<std::pair<uint32_t, uint32_t>> rewires;   // (parent, new only child)
-    std::vector<uint32_t> path;
-
-    for (const auto& p : t.patterns) {
-        const uint32_t L = uint32_t(p.size());
-        if (L < 4) continue;
-        path.assign(1, 0u);
-        for (unsigned char ch : p) {
-            uint32_t nx = child_by_sym(path.back(), uint32_t(a.symbol_of(ch)));
-            if (nx == Trie::kNone) fail(HEPFAC_ERR_INTERNAL, "pattern missing from trie");
-            path.push_back(nx);
-        }
-        // Longest eligible chain: path[L-k] unary & non-terminal, the deepest one
-        // pointing at a shared (leaf) terminal.
+    // Phase A (parallel, per pattern): its path's last nodes and the length
+    // of its eligible tail chain.  Phase B (serial, pattern order) assigns the
+    // class representatives, which depends on which pattern comes first.
+    struct Tail {
         uint32_t chain = 0;
-        for (uint32_t k = 1; k <= 3; ++k) {
-            const uint32_t v = path[L - k];
-            if (g.term[v] || g.degree[v] != 1) break;
-            if (k == 1 && !leaf_terminal(g.only_child(v))) break;
-            chain = k;
+        uint32_t node[5] = {0, 0, 0, 0, 0}; // path[L - k] for k = 0..4
+    };
+    const size_t P = t.patterns.size();
+    std::vector<Tail> tails(P);
+    std::vector<uint8_t> missing(P, 0);
+    parallel_slices(P, 8192, [&](size_t b, size_t e) {
+        std::vector<uint32_t> path;
+        for (size_t i = b; i < e; ++i) {
+            const std::string& p = t.patterns[i];
+            const uint32_t L = uint32_t(p.size());
+            if (L < 4) continue;
+            path.assign(1, 0u);
+            for (unsigned char ch : p) {
+                const uint32_t nx = child_by_sym(path.back(), uint32_t(a.symbol_of(ch)));
+                if (nx == Trie::kNone) {
+                    missing[i] = 1;
+                    break;
+                }
+                path.push_back(nx);
+            }
+            if (missing[i]) continue;
+            // Longest eligible chain: path[L-k] unary & non-terminal, the
+            // deepest one pointing at a shared (leaf) terminal.
+            uint32_t chain = 0;
+            for (uint32_t k = 1; k <= 3; ++k) {
+                const uint32_t v = path[L - k];
+                if (g.term[v] || g.degree[v] != 1) break;
+                if (k == 1 && !leaf_terminal(g.only_child(v))) break;
+                chain = k;
+            }
+            // The edge into the chain head must belong to a unary parent.
+            while (chain >= 1 && g.degree[path[L - chain - 1]] > 1) --chain;
+            tails[i].chain = chain;
+            for (uint32_t k = 0; k <= 4; ++k) tails[i].node[k] = path[L - k];
         }
-        // The edge into the chain head must belong to a unary parent.
-        while (chain >= 1 && g.degree[path[L - chain - 1]] > 1) --chain;
-        if (chain == 0) continue;
+    });
+    for (size_t i = 0; i < P; ++i)
+        if (missing[i]) fail(HEPFAC_ERR_INTERNAL, "pattern missing from trie");
 
+    for (size_t i = 0; i < P; ++i) {
+        const std::string& p = t.patterns[i];
+        const uint32_t chain = tails[i].chain;
+        if (chain == 0) continue;
+        const uint32_t* node = tails[i].node; // node[k] = path[L - k]
         uint32_t replace = 0; // deepest level whose class already has another owner
         for (uint32_t k = chain; k >= 1; --k) {
             auto it = rep_of_suffix.find(suffix_key(p, k));
-            if (it != rep_of_suffix.end() && it->second != path[L - k]) {
+            if (it != rep_of_suffix.end() && it->second != node[k]) {
                 replace = k;
                 break;
             }
         }
         for (uint32_t k = replace + 1; k <= chain; ++k) {
             const uint32_t key = suffix_key(p, k);
-            if (rep_of_suffix.emplace(key, path[L - k]).second) reps.emplace_back(path[L - k], key);
+            if (rep_of_suffix.emplace(key, node[k]).second) reps.emplace_back(node[k], key);
         }
         if (replace >= 1)
-            rewires.emplace_back(path[L - replace - 1], rep_of_suffix.at(suffix_key(p, replace)));
+            rewires.emplace_back(node[replace + 1], rep_of_suffix.at(suffix_key(p, replace)));
     }
 
     // Representatives of k-suffixes point at the representative of their
