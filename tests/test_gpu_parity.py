@@ -297,3 +297,24 @@ def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth):
     monkeypatch.setenv("HEPFAC_CHUNK_MIB", "64")
     assert same(gpu.scan(t, tx), want)
     assert gpu.last_scan_stats()["chunks"] == 1
+
+
+@pytest.mark.parametrize("stages,depth", [(1, 4), (2, None)])
+def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth):
+    # Every start of a run of 'A's passes both pair levels and the prefix
+    # recheck: exercises the filter pass's per-chunk fallback (a step with more
+    # candidates than its queue), candidate-region overflow and re-run, and
+    # walk units with more candidates than a warp queue.
+    monkeypatch.setenv("HEPFAC_FILTER_MODE", "pair")
+    rng = np.random.default_rng(31)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 1000, 4, 24)
+    pats = sorted(set(pats) | {b"AAAA", b"AAAAB", b"AAAAAAAA", b"AAAAAAAAAAAAAAAAAAAAAAAAAAAAAA"})
+    t = build(gpu, pats, 256, stages, depth)
+    assert gpu.layout_info(t)["filter_mode"] == 2
+    tx = np.frombuffer(b"A" * 400000, dtype=np.uint8).copy()
+    tx[123456:123456 + 4096] = text(rng, syms, 4096)
+    for i, p in enumerate(pats[:200]):
+        plant(tx, p, 200000 + i * 97)
+    got = gpu.scan(t, tx)
+    assert same(got, oracle.naive_find_all(tx, pats))
