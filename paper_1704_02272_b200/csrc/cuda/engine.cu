@@ -112,7 +112,9 @@ struct DeviceTrie {
     TrieView view{};
     bool grouped = false, identity = false;
     int kw = 0;
-    bool pair = false;
+    bool pair = false;          // two-pass pipeline: filter pass + candidate-walking pass
+    bool lean_single = false;   // its filter pass is the single-probe form
+    void (*filter_fn)(gpu::FilterArgs) = nullptr;
     double filter_pass = 1.0;
     KernelFn kernel = nullptr;
     size_t smem = 0;
@@ -230,16 +232,18 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.jump_bits = im.jump_bits;
     v.min_emit = im.min_emit;
 
-    d->pair = im.filter_mode == 2 && pair_pipeline_enabled();
+    d->lean_single = im.filter_mode == 1 && im.lean_single;
+    d->pair = (im.filter_mode == 2 || d->lean_single) && pair_pipeline_enabled();
     if (d->pair) {
+        d->filter_fn = !d->lean_single ? gpu::pfac_pair_filter_kernel
+                                       : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3> : gpu::pfac_single_filter_kernel<2>);
         d->kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
         d->warps = gpu::kCWarps;
-        d->filter_smem = size_t(v.filter_words) * 4 + gpu::filter_smem_fixed_bytes();
-        CK(cudaFuncSetAttribute(gpu::pfac_pair_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(d->filter_smem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, gpu::pfac_pair_filter_kernel,
-                                                         gpu::kFThreads, d->filter_smem));
+        d->filter_smem = size_t(v.filter_words) * 4 + (d->lean_single ? 0 : gpu::filter_smem_fixed_bytes());
+        CK(cudaFuncSetAttribute(d->filter_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->filter_smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
+                                                         d->filter_smem));
         if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
     } else {
         d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
@@ -483,8 +487,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         const uint64_t fgrid = uint64_t(dt.sm_count) * dt.filter_blocks_per_sm;
         const uint64_t fwarps = fgrid * gpu::kFWarps;
         ws.ensure_ctiles(l.n_ftiles);
-        // expected: ~0.2% of starts survive; regions grow on overflow
-        if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / 256 / fwarps + 256);
+        // expected: <= ~1% of starts survive; regions grow on overflow
+        if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / (dt.lean_single ? 64 : 256) / fwarps + 256);
         ws.ensure_cand(fwarps, ws.cand_cap);
         gpu::FilterArgs f{};
         f.table = dt.view.filter;
@@ -501,7 +505,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.tile_ccount = ws.d_tile_ccount;
         f.tile_cslot = ws.d_tile_cslot;
         f.cand_need = ws.d_small + 5;
-        gpu::pfac_pair_filter_kernel<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
+        f.filter_k = dt.view.filter_k;
+        dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());
         if (between) CK(cudaEventRecord(between, ws.stream));
         a.cand = ws.d_cand;
@@ -723,7 +728,7 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
-    li.filter_mode = d->kw == 0 ? 0u : (d->pair ? 2u : 1u);
+    li.filter_mode = d->kw == 0 ? 0u : ((d->pair && !d->lean_single) ? 2u : 1u);
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }

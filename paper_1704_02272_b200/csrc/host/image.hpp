@@ -30,6 +30,7 @@ struct GpuImage {
 
     uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
     uint32_t filter_mode = 0; // 0 none, 1 single probe, 2 pair probes (layout.hpp)
+    bool lean_single = false; // single probe, few survivors: two-pass pipeline (filter pass + walking pass)
     uint32_t pair_shift = 0;
     double filter_pass = 1.0; // estimated fraction of random starts reaching the walk queue
     uint64_t filter_paths = 0;
@@ -52,6 +53,7 @@ struct ImageOptions {
     uint32_t max_filter2_bits = 27; // 16 MiB in global memory
     bool jump = true;               // depth-k jump table (HEPFAC_JUMP=0 disables)
     uint32_t filter_mode = 0;       // 0 = cost model, 1 = single, 2 = pair (HEPFAC_FILTER_MODE)
+    bool lean_single = false;       // selective single-probe tries on the two-pass pipeline (HEPFAC_LEAN_SINGLE)
 };
 
 ImageOptions image_options_from_env();

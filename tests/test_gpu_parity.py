@@ -318,3 +318,18 @@ def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth):
         plant(tx, p, 200000 + i * 97)
     got = gpu.scan(t, tx)
     assert same(got, oracle.naive_find_all(tx, pats))
+
+
+@pytest.mark.parametrize("stages,depth", [(1, 5), (2, None)])
+def test_lean_single_pipeline(gpu, monkeypatch, stages, depth):
+    # the opt-in single-probe two-pass pipeline (HEPFAC_LEAN_SINGLE=1, k >= 4)
+    monkeypatch.setenv("HEPFAC_LEAN_SINGLE", "1")
+    monkeypatch.setenv("HEPFAC_FILTER_MODE", "single")
+    rng = np.random.default_rng(33)
+    a, syms = alphabet_bytes(gpu, 20)
+    pats = pattern_set(rng, syms, 2000, 6, 20)
+    t = build(gpu, pats, 20, stages, depth)
+    tx = text(rng, syms, 1 << 20)
+    for i, p in enumerate(pats):
+        plant(tx, p, (i * 331) % (tx.size - 24))
+    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
