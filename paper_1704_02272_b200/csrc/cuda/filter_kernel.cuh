@@ -106,7 +106,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
     const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
     uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
     uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
-    uint64_t cursor = 0;
+    // 32-bit cursors: a warp's region never holds more entries than its
+    // starts (< 2^32 unless the text is > 4736 x 4 Gi bytes)
+    const uint32_t cap = uint32_t(min(a.cand_cap, uint64_t(0xFFFFFFFFu)));
+    uint32_t cursor = 0;
     const uint32_t below = (1u << lane) - 1u;
     static_assert(kFChunks * kFStageStride <= 2112, "staging offset -> chunk division assumes 4 chunks of 528 B");
 
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
 
     for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
         const uint64_t lo = tile * kFTile;
-        const uint64_t slot = cursor;
+        const uint32_t slot = cursor;
         const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
         const uint32_t steps = (rem + kFStep - 1) / kFStep;
         uint4 nxt[kFChunks];
@@ -220,8 +223,8 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                     }
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
                     if (keep) {
-                        const uint64_t at = cursor + __popc(bal & below);
-                        if (at < a.cand_cap) {
+                        const uint32_t at = cursor + __popc(bal & below);
+                        if (at < cap) {
                             const uint32_t c = (so * 125u) >> 16; // so / 528 for every valid so < 2112
                             region[at] = uint16_t(s * kFStep + so - 16u * c);
                             keys[at] = y;
@@ -239,11 +242,11 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             }
         }
         if (lane == 0) {
-            a.tile_ccount[tile] = uint32_t(cursor - slot);
+            a.tile_ccount[tile] = cursor - slot;
             a.tile_cslot[tile] = uint32_t(slot);
         }
     }
-    if (lane == 0 && cursor > a.cand_cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+    if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
 }
 
 constexpr uint32_t filter_smem_fixed_bytes() { return kFWarps * kFWarpSmem; }
