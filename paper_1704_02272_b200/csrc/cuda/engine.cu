@@ -118,9 +118,14 @@ struct DeviceTrie {
     double filter_pass = 1.0;
     KernelFn kernel = nullptr;
     size_t smem = 0;
-    // pair pipeline: filter pass, then the candidate-walking pass (`kernel`)
+    // two-pass pipeline (pair tries, texts >= pipeline_min): filter pass,
+    // then the candidate-walking pass; smaller texts use the one-pass `kernel`
     size_t filter_smem = 0;
     int filter_blocks_per_sm = 0;
+    KernelFn walk_kernel = nullptr;
+    size_t walk_smem = 0;
+    int walk_blocks_per_sm = 1;
+    uint64_t pipeline_min = 0;
     int blocks_per_sm = 1, sm_count = 1;
     uint32_t warps = gpu::kWarps; // per CTA of `kernel`
     uint32_t min_emit = UINT32_MAX, node_count = 0, groups = 0;
@@ -152,6 +157,20 @@ bool pair_pipeline_enabled()
 {
     const char* s = std::getenv("HEPFAC_PAIR_PIPELINE");
     return !s || std::strtol(s, nullptr, 10) != 0;
+}
+
+// Launches covering fewer starts than this use the one-pass kernel: the
+// two-pass pipeline has ~35 us more fixed cost (a second launch, grid
+// barriers over more warps), and wins only above ~225 MiB (c3 measurements).
+// HEPFAC_PIPELINE_MIN_MIB overrides (0 = always pipeline).
+uint64_t pipeline_min_bytes()
+{
+    uint64_t mib = 256;
+    if (const char* s = std::getenv("HEPFAC_PIPELINE_MIN_MIB")) {
+        const long v = std::strtol(s, nullptr, 10);
+        if (v >= 0) mib = uint64_t(v);
+    }
+    return mib << 20;
 }
 
 KernelFn select_kernel(bool grouped, bool identity, int kw, bool pair)
@@ -233,25 +252,30 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.min_emit = im.min_emit;
 
     d->lean_single = im.filter_mode == 1 && im.lean_single;
+    // one-pass (fused) kernel: always available
+    d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
+    d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
+    CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
+    d->blocks_per_sm = std::max(1, d->blocks_per_sm);
+    // two-pass pipeline
     d->pair = (im.filter_mode == 2 || d->lean_single) && pair_pipeline_enabled();
     if (d->pair) {
+        d->pipeline_min = pipeline_min_bytes();
         d->filter_fn = !d->lean_single ? gpu::pfac_pair_filter_kernel
                                        : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3> : gpu::pfac_single_filter_kernel<2>);
-        d->kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
-        d->smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
-        d->warps = gpu::kCWarps;
+        d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
+        d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
+        CK(cudaFuncSetAttribute(d->walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->walk_smem)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->walk_blocks_per_sm, d->walk_kernel,
+                                                         int(gpu::kCWarps * 32), d->walk_smem));
+        d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         d->filter_smem = size_t(v.filter_words) * 4 + (d->lean_single ? 0 : gpu::filter_smem_fixed_bytes());
         CK(cudaFuncSetAttribute(d->filter_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->filter_smem)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
                                                          d->filter_smem));
         if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
-    } else {
-        d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
-        d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
     }
-    CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
-    d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     CK(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device));
     return d;
 }
@@ -433,17 +457,20 @@ struct Launch {
     uint64_t n_ftiles = 0; // pair pipeline: filter tiles (n_tiles counts walk units of kSuper of them)
 };
 
+bool pipelined(const DeviceTrie& dt, uint64_t n_own) { return dt.pair && n_own >= dt.pipeline_min; }
+
 Launch plan(const DeviceTrie& dt, uint64_t n_own)
 {
     Launch l;
     l.n_tiles = (n_own + gpu::kTile - 1) / gpu::kTile;
-    if (dt.pair) {
+    const bool two = pipelined(dt, n_own);
+    if (two) {
         l.n_ftiles = l.n_tiles;
         l.n_tiles = (l.n_ftiles + gpu::kSuper - 1) / gpu::kSuper;
     }
-    l.grid = std::min<uint64_t>(uint64_t(dt.sm_count) * dt.blocks_per_sm,
-                                std::max<uint64_t>(1, (l.n_tiles + dt.warps - 1) / dt.warps));
-    l.warps = l.grid * dt.warps;
+    const uint64_t warps = two ? gpu::kCWarps : dt.warps, bps = two ? dt.walk_blocks_per_sm : dt.blocks_per_sm;
+    l.grid = std::min<uint64_t>(uint64_t(dt.sm_count) * bps, std::max<uint64_t>(1, (l.n_tiles + warps - 1) / warps));
+    l.warps = l.grid * warps;
     return l;
 }
 
@@ -483,7 +510,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
     a.base_out = base_out;
     a.warp_need = ws.d_small;
     a.err = reinterpret_cast<unsigned int*>(ws.d_small + 2);
-    if (dt.pair) {
+    const bool two = pipelined(dt, n_own);
+    if (two) {
         const uint64_t fgrid = uint64_t(dt.sm_count) * dt.filter_blocks_per_sm;
         const uint64_t fwarps = fgrid * gpu::kFWarps;
         ws.ensure_ctiles(l.n_ftiles);
@@ -523,13 +551,14 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         CK(cudaMemsetAsync(ws.d_small + 6, 0, sizeof(unsigned long long), ws.stream));
     }
     void* params[] = {&a};
-    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.kernel), dim3(unsigned(l.grid)),
-                                                      dim3(dt.warps * 32), params, dt.smem, ws.stream);
+    const cudaError_t e = cudaLaunchCooperativeKernel(
+        reinterpret_cast<const void*>(two ? dt.walk_kernel : dt.kernel), dim3(unsigned(l.grid)),
+        dim3((two ? gpu::kCWarps : dt.warps) * 32), params, two ? dt.walk_smem : dt.smem, ws.stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         cuda_fail(e, "pfac_scan_kernel launch");
     }
-    return dt.pair ? 2 : 1;
+    return two ? 2 : 1;
 }
 
 // Reads back the scan's accumulators; true when the results are complete.
@@ -550,7 +579,7 @@ bool fetch_small(Workspace& ws, const DeviceTrie& dt, uint64_t n_own, const unsi
         ok = false;
     }
     if (ws.h_small[5]) { // some filter warp's candidate region overflowed
-        const uint64_t fwarps = uint64_t(dt.sm_count) * dt.filter_blocks_per_sm * gpu::kFWarps;
+        const uint64_t fwarps = uint64_t(dt.sm_count) * std::max(1, dt.filter_blocks_per_sm) * gpu::kFWarps;
         ws.ensure_cand(fwarps, ws.h_small[5] + ws.h_small[5] / 4 + 256);
         ok = false;
     }
@@ -834,7 +863,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventRecord(s->evs[3 * i + 2], ws.stream));
     }
     s->last_iterations = iterations;
-    s->split = can_match && dt.pair;
+    s->split = can_match && pipelined(dt, s->owned);
     s->complete = !can_match || fetch_small(ws, dt, s->owned); // grows buffers for the next run
     s->matches = can_match ? records_of(ws) : 0;
     for (uint32_t i = 0; i < iterations; ++i)
@@ -844,7 +873,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
 void session_split(Session* s, uint32_t n, double* first_ms, double* second_ms, uint32_t* kernels_per_scan)
 {
     DeviceGuard g(s->ws->device);
-    if (kernels_per_scan) *kernels_per_scan = s->dt->pair ? 2u : 1u;
+    if (kernels_per_scan) *kernels_per_scan = pipelined(*s->dt, s->owned) ? 2u : 1u;
     n = std::min(n, s->last_iterations);
     for (uint32_t i = 0; i < n; ++i) {
         const double total = elapsed_ms(s->evs[3 * i], s->evs[3 * i + 2]);

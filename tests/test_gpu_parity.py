@@ -61,9 +61,13 @@ def test_empty_and_tiny_texts(gpu):
     assert as_tuples(gpu.scan(t, b"ABC")) == [(0, 3, 0)]
 
 
+@pytest.mark.parametrize("two_pass", [False, True])
 @pytest.mark.parametrize("sigma", [2, 4, 20, 52, 64, 128, 256])
-def test_random_instances_all_states(gpu, sigma):
+def test_random_instances_all_states(gpu, monkeypatch, sigma, two_pass):
     # acceptance criteria 3 + 4 shape: random sets, planted + boundary copies.
+    # two_pass: pair-filter tries on the two-pass pipeline even for small texts
+    if two_pass:
+        monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(1000 + sigma)
     a, syms = alphabet_bytes(gpu, sigma)
     for rep in range(6):
@@ -272,11 +276,14 @@ def test_foreign_terminal_is_reported(gpu, tmp_path):
     assert gpu.scan(bad, b"xxXYZWyy").size == 1
 
 
+@pytest.mark.parametrize("two_pass", [False, True])
 @pytest.mark.parametrize("sigma,stages,depth", [(256, 2, None), (4, 1, 5), (256, 0, 3)])
-def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth):
+def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth, two_pass):
     # hepfac_scan streams texts longer than two chunks (H2D of chunk c+1 under
     # the kernel of chunk c, device-side running output base); 1 MiB chunks
     # force many chunk seams, planted matches straddle them.
+    if two_pass:
+        monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(sigma + 7)
     a, syms = alphabet_bytes(gpu, sigma)
     pats = pattern_set(rng, syms, 300, 4, 40)
@@ -306,6 +313,7 @@ def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth):
     # candidates than its queue), candidate-region overflow and re-run, and
     # walk units with more candidates than a warp queue.
     monkeypatch.setenv("HEPFAC_FILTER_MODE", "pair")
+    monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(31)
     syms = np.arange(256, dtype=np.uint8)
     pats = pattern_set(rng, syms, 1000, 4, 24)
@@ -325,6 +333,7 @@ def test_lean_single_pipeline(gpu, monkeypatch, stages, depth):
     # the opt-in single-probe two-pass pipeline (HEPFAC_LEAN_SINGLE=1, k >= 4)
     monkeypatch.setenv("HEPFAC_LEAN_SINGLE", "1")
     monkeypatch.setenv("HEPFAC_FILTER_MODE", "single")
+    monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(33)
     a, syms = alphabet_bytes(gpu, 20)
     pats = pattern_set(rng, syms, 2000, 6, 20)
