@@ -196,11 +196,16 @@ __device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint6
 __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, Sink& sink)
 {
     const TrieView& t = a.trie;
+    // Every bucket pattern spells the node's depth-limit path (the walk just
+    // matched it), so the compare starts at the last 4-byte boundary before
+    // the limit (pattern bytes are stored 4-byte aligned).
+    const uint32_t skip = t.depth_limit & ~3u;
     const uint2 span = __ldg(reinterpret_cast<const uint2*>(t.bk_span) + __ldg(t.bucket_of + node));
     for (uint32_t k = span.x, e = span.x + span.y; k < e; ++k) {
         const uint4 en = __ldg(reinterpret_cast<const uint4*>(t.bk_entry) + k);
         if (start + en.y > a.n_avail) continue; // overhangs the text end (scan.cpp:43)
-        if (same_at(a, start, (uint64_t(en.w) << 32) | en.z, en.y)) sink.put(a.g0 + start, en.y, en.x);
+        if (same_at(a, start + skip, ((uint64_t(en.w) << 32) | en.z) + skip, en.y - skip))
+            sink.put(a.g0 + start, en.y, en.x);
     }
 }
 
