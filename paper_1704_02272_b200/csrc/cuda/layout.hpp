@@ -93,8 +93,13 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 // Jump table: every depth-k path string (k = filter_k bytes, little-endian in
 // {lo, hi}) -> the node it reaches.  No node above depth k can report
 // (k <= min_emit), so a walk may start there instead of at the root.  Open
-// addressing, load <= 1/2, 16-byte slots {lo, hi, node, 0}; node == kNoId
-// marks an empty slot.
+// addressing, load <= 1/2, 32-byte slots
+//   {lo, hi, node, term, bk_first, bk_count, flags, 0}
+// node == kNoId marks an empty slot.  The rest describes the node itself, so a
+// walk that starts at the depth limit (truncated tries with k == limit) emits
+// without reading the node record or the bucket index: term = its private
+// pattern id (kNoId = resolve by key), flags bit 0 terminal, bit 1 bucket.
+constexpr uint32_t kJumpWords = 8;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 
 // Device view of an uploaded image (plain pointers, passed by value).

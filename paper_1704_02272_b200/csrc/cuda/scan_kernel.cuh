@@ -193,20 +193,25 @@ __device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint6
 // Depth-limit verification (scan.cpp:37-49): bucket entries are pre-sorted by
 // (length, id), which is the order the records must appear in.  One load
 // gives the bucket's span, one load per entry its id, length and bytes.
-__device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, Sink& sink)
+__device__ __forceinline__ void verify_span(const ScanArgs& a, uint2 span, uint64_t start, Sink& sink)
 {
     const TrieView& t = a.trie;
     // Every bucket pattern spells the node's depth-limit path (the walk just
     // matched it), so the compare starts at the last 4-byte boundary before
     // the limit (pattern bytes are stored 4-byte aligned).
     const uint32_t skip = t.depth_limit & ~3u;
-    const uint2 span = __ldg(reinterpret_cast<const uint2*>(t.bk_span) + __ldg(t.bucket_of + node));
     for (uint32_t k = span.x, e = span.x + span.y; k < e; ++k) {
         const uint4 en = __ldg(reinterpret_cast<const uint4*>(t.bk_entry) + k);
         if (start + en.y > a.n_avail) continue; // overhangs the text end (scan.cpp:43)
         if (same_at(a, start + skip, ((uint64_t(en.w) << 32) | en.z) + skip, en.y - skip))
             sink.put(a.g0 + start, en.y, en.x);
     }
+}
+
+__device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, Sink& sink)
+{
+    const TrieView& t = a.trie;
+    verify_span(a, __ldg(reinterpret_cast<const uint2*>(t.bk_span) + __ldg(t.bucket_of + node)), start, sink);
 }
 
 // One failure-less walk (scan.cpp:20-51).  Each step issues a single record
@@ -461,10 +466,14 @@ __device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
     return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
 }
 
-// The node a start reaches after its first k bytes (`win` = text[start,
-// start + 8)), or kNoId when no trie path spells them.
+// The jump-table slot of the node a start reaches after its first k bytes
+// (`win` = text[start, start + 8)); w.z == kNoId when no trie path spells them.
+struct JumpHit {
+    uint4 w;   // {lo, hi, node, term}
+    uint4 aux; // {bk_first, bk_count, flags, 0}
+};
 template <int KW>
-__device__ __forceinline__ uint32_t jump_node(const TrieView& t, uint64_t win)
+__device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
 {
     const uint32_t k = t.filter_k;
     uint32_t lo = uint32_t(win), hi = 0;
@@ -473,9 +482,26 @@ __device__ __forceinline__ uint32_t jump_node(const TrieView& t, uint64_t win)
     const uint32_t mask = (1u << t.jump_bits) - 1u;
     const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
     for (uint32_t s = jump_slot(lo ^ (hi * 0x85EBCA77u), t.jump_bits);; s = (s + 1) & mask) {
-        const uint4 e = __ldg(slots + s);
-        if (e.z == kNoId || (e.x == lo && e.y == hi)) return e.z;
+        JumpHit h;
+        h.w = __ldg(slots + 2 * s);
+        h.aux = __ldg(slots + 2 * s + 1); // same 32-byte sector: no extra latency
+        if (h.w.z == kNoId || (h.w.x == lo && h.w.y == hi)) return h;
     }
+}
+
+// A walk that starts at the depth limit (k == limit): the node's terminal
+// record and its bucket come from the jump slot (walk() semantics at the
+// limit: terminal first, then the bucket in (length, id) order).
+__device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& h, uint64_t start, uint32_t depth,
+                                              Sink& sink)
+{
+    if (h.aux.z & 1u) {
+        uint32_t id = h.w.w;
+        if (id == kNoId) id = resolve_slice(a, start, depth);
+        if (id == kNoId) atomicOr(a.err, 1u);
+        else sink.put(a.g0 + start, depth, id);
+    }
+    if (h.aux.z & 2u) verify_span(a, make_uint2(h.aux.x, h.aux.y), start, sink);
 }
 
 template <bool GROUPED, bool IDENT, int KW>
@@ -522,14 +548,21 @@ struct Walker {
             uint64_t start = 0;
             uint64_t win = 0;
             uint32_t node = 0, depth = 0;
+            JumpHit hit{};
+            // k == limit: walks end at the jump node; the slot has what they emit
+            const bool at_limit = KW != 0 && a.trie.jump_bits && a.trie.filter_k == a.trie.depth_limit;
             if (e < ns) {
                 start = lo + q[e];
                 win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
                 if (KW != 0 && a.trie.jump_bits) {
-                    node = jump_node<KW>(a.trie, win);
+                    hit = jump_lookup<KW>(a.trie, win);
+                    node = hit.w.z;
                     depth = a.trie.filter_k;
                 }
-                if (node != kNoId) walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, sink);
+                if (node != kNoId) {
+                    if (at_limit) emit_at_limit(a, hit, start, depth, sink);
+                    else walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, sink);
+                }
             }
             uint32_t tot;
             const uint32_t ex = warp_exclusive(sink.n, lane, tot);
@@ -544,7 +577,8 @@ struct Walker {
                     wr.at = at + kRegRecords;
                     wr.cap = a.warp_cap;
                     wr.skip = kRegRecords;
-                    walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, wr);
+                    if (at_limit) emit_at_limit(a, hit, start, depth, wr);
+                    else walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, wr);
                 }
             }
             cursor += tot;

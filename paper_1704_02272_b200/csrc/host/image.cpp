@@ -412,21 +412,29 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 const uint32_t jb = std::max<uint32_t>(ceil_log2(grams.size()) + 1, 4);
                 const uint32_t mask = (1u << jb) - 1u;
                 im.jump_bits = jb;
-                im.jump.assign(size_t(4) << jb, 0u);
-                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[4 * s + 2] = kNoId;
+                constexpr size_t W = kJumpWords;
+                im.jump.assign(W << jb, 0u);
+                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[W * s + 2] = kNoId;
                 for (size_t i = 0; i < grams.size(); ++i) {
                     uint32_t s = jump_slot(filter_fold(grams[i]), jb);
-                    while (im.jump[4 * s + 2] != kNoId) s = (s + 1) & mask;
-                    im.jump[4 * s + 0] = uint32_t(grams[i]);
-                    im.jump[4 * s + 1] = uint32_t(grams[i] >> 32);
-                    im.jump[4 * s + 2] = gram_node[i];
+                    while (im.jump[W * s + 2] != kNoId) s = (s + 1) & mask;
+                    const uint32_t node = gram_node[i];
+                    uint32_t* slot = &im.jump[W * s];
+                    slot[0] = uint32_t(grams[i]);
+                    slot[1] = uint32_t(grams[i] >> 32);
+                    slot[2] = node;
+                    slot[3] = im.term_id[node];
+                    const uint32_t b = im.bucket_of[node];
+                    slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
+                    slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
+                    slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
                 }
             }
         }
     }
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
-    if (im.jump.empty()) im.jump.assign(4, 0u);
+    if (im.jump.empty()) im.jump.assign(kJumpWords, 0u);
 
     for (uint32_t u = 0; u < n; ++u)
         if (t.terminal(u) && u != 0) (im.term_id[u] == kNoId ? im.keyed_terminals : im.private_terminals)++;
