@@ -330,12 +330,13 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             }
             // Pass rates on text drawn uniformly from the alphabet (Monte Carlo,
             // fixed seed): what fraction of starts survive each level.
-            double p_single = f_single, p_first = f_pair, p_both = f_pair * f_pair;
+            double p_single = f_single, p_first = f_pair, p_both = f_pair * f_pair, p_true = 0.0;
             {
                 const uint32_t sigma = t.alphabet.size();
                 const uint32_t N = 1u << 15;
                 uint64_t x = 0x9E3779B97F4A7C15ull;
-                uint32_t n_single = 0, n_first = 0, n_both = 0;
+                uint32_t n_single = 0, n_first = 0, n_both = 0, n_true = 0;
+                const std::unordered_set<uint64_t> paths(grams.begin(), grams.end());
                 auto word_bit = [](const std::vector<uint32_t>& tab, uint32_t word, uint32_t byte) {
                     return (tab[word] & filter_mask_bit(byte)) != 0;
                 };
@@ -347,6 +348,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     }
                     const uint32_t k32 = filter_fold(key);
                     n_single += word_bit(single, filter_word(k32, bits - 5), k32);
+                    n_true += paths.count(key) ? 1u : 0u;
                     if (k >= 4) {
                         const uint32_t p = uint32_t(key);
                         const bool a = word_bit(pair, pair_word(p >> 8, pair_wb), p & 0xFFu);
@@ -356,6 +358,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     }
                 }
                 p_single = double(n_single) / N;
+                p_true = double(n_true) / N;
                 if (k >= 4) p_first = double(n_first) / N, p_both = double(n_both) / N;
             }
             // Cost per start in issue slots (shared-memory wavefronts counted
@@ -398,7 +401,11 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             }
             // Third level (L2-resident, whole k-byte key) when what reaches the
             // walk queue is still dense.
-            if (im.filter_mode == 1 || im.filter_pass > 0.002) {
+            // ... unless most of what passes are real depth-k paths (small
+            // alphabets: DNA 14% of 16.6%): the jump table is exact, and one
+            // more L2 round trip per survivor would filter almost nothing.
+            const bool mostly_true = p_true > 0.5 * im.filter_pass;
+            if ((im.filter_mode == 1 || im.filter_pass > 0.002) && !mostly_true) {
                 const uint32_t bits2 =
                     std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter2_slack, 16, opt.max_filter2_bits);
                 im.filter2_bits = bits2;
