@@ -170,7 +170,10 @@ def test_text_sizes_around_tiles(gpu):
         assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats)), n
 
 
-def test_shards_concatenate_to_full_scan(gpu):
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_shards_concatenate_to_full_scan(gpu, monkeypatch, two_pass):
+    if two_pass:
+        monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(21)
     syms = np.arange(256, dtype=np.uint8)
     pats = pattern_set(rng, syms, 500, 2, 24)
@@ -203,7 +206,10 @@ def test_run_throughput_report(gpu):
     assert rep["matches"] == gpu.scan(t, tx).size
 
 
-def test_session_device_resident(gpu):
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_session_device_resident(gpu, monkeypatch, two_pass):
+    if two_pass:
+        monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(8)
     syms = np.arange(256, dtype=np.uint8)
     pats = pattern_set(rng, syms, 2000, 4, 32)
@@ -214,6 +220,10 @@ def test_session_device_resident(gpu):
     s = gpu.session(t, tx)
     ms, m = s.run(3)
     assert len(ms) == 3 and all(x > 0 for x in ms)
+    first, second, kernels = s.kernel_ms(3)
+    assert kernels == (2 if two_pass else 1)
+    assert all(abs(f + g - x) < 1e-3 for f, g, x in zip(first, second, ms))
+    assert all(g > 0 for g in second) if two_pass else all(g == 0 for g in second)
     assert same(s.fetch(), oracle.naive_find_all(tx, pats))
     s.close()
 
