@@ -126,6 +126,8 @@ struct DeviceTrie {
     size_t walk_smem = 0;
     int walk_blocks_per_sm = 1;
     uint64_t pipeline_min = 0;
+    uint32_t sym_bits = 0; // symbol-key mode: the text is packed before the filter pass
+    void (*pack_fn)(const uint8_t*, uint64_t, const uint16_t*, uint32_t*) = nullptr;
     int blocks_per_sm = 1, sm_count = 1;
     uint32_t warps = gpu::kWarps; // per CTA of `kernel`
     uint32_t min_emit = UINT32_MAX, node_count = 0, groups = 0;
@@ -239,6 +241,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_words = d->kw ? uint32_t(im.filter.size()) : 0u;
     v.filter_bits = im.filter_bits;
     v.filter_k = im.filter_k;
+    v.sym_bits = im.sym_bits;
     v.pair_shift = im.pair_shift;
     v.pair_mul = im.pair_shift ? 1u << (32 - im.pair_shift) : 0u;
     v.mul_shr8 = 1u << 24;
@@ -258,19 +261,31 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
-    // two-pass pipeline
-    d->pair = (im.filter_mode == 2 || d->lean_single) && pair_pipeline_enabled();
+    // two-pass pipeline (always for symbol keys: the one-pass kernel reads byte keys)
+    d->sym_bits = im.sym_bits;
+    d->pair = ((im.filter_mode == 2 || d->lean_single) && pair_pipeline_enabled()) || im.filter_mode == 3;
     if (d->pair) {
-        d->pipeline_min = pipeline_min_bytes();
-        d->filter_fn = !d->lean_single ? gpu::pfac_pair_filter_kernel
-                                       : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3> : gpu::pfac_single_filter_kernel<2>);
+        d->pipeline_min = im.filter_mode == 3 ? 0 : pipeline_min_bytes();
+        if (im.filter_mode == 3) {
+            d->filter_fn = im.sym_bits == 1 ? gpu::pfac_symbol_filter_kernel<1>
+                                            : (im.sym_bits == 2 ? gpu::pfac_symbol_filter_kernel<2>
+                                                                : gpu::pfac_symbol_filter_kernel<4>);
+            d->pack_fn = im.sym_bits == 1 ? gpu::pfac_pack_symbols_kernel<1>
+                                          : (im.sym_bits == 2 ? gpu::pfac_pack_symbols_kernel<2>
+                                                              : gpu::pfac_pack_symbols_kernel<4>);
+        } else {
+            d->filter_fn = !d->lean_single ? gpu::pfac_pair_filter_kernel
+                                           : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3>
+                                                         : gpu::pfac_single_filter_kernel<2>);
+        }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
         CK(cudaFuncSetAttribute(d->walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->walk_smem)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->walk_blocks_per_sm, d->walk_kernel,
                                                          int(gpu::kCWarps * 32), d->walk_smem));
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
-        d->filter_smem = size_t(v.filter_words) * 4 + (d->lean_single ? 0 : gpu::filter_smem_fixed_bytes());
+        d->filter_smem = size_t(v.filter_words) * 4 +
+                         ((d->lean_single || im.filter_mode == 3) ? 0 : gpu::filter_smem_fixed_bytes());
         CK(cudaFuncSetAttribute(d->filter_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->filter_smem)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
                                                          d->filter_smem));
@@ -326,6 +341,8 @@ struct Workspace {
     uint64_t ctile_cap = 0, ctile_cap2 = 0;
     uint32_t* d_tile_region = nullptr;
     uint64_t region_cap = 0;
+    uint32_t* d_packed = nullptr; // symbol-key mode: the packed text
+    uint64_t packed_cap = 0;
     // [0] max records a warp needed (0 = fits), [1] total of the last launch,
     // [2] error word, [3] zero (base_in of a single launch), [4] its base_out,
     // [5] max candidates a filter warp needed (0 = fits), [6] dynamic unit counter
@@ -355,7 +372,7 @@ struct Workspace {
         for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
                         (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
                         (void*)d_flush, (void*)d_cand, (void*)d_cand_key, (void*)d_tile_ccount, (void*)d_tile_cslot,
-                        (void*)d_tile_region})
+                        (void*)d_tile_region, (void*)d_packed})
             cudaFree(p);
         cudaFreeHost(h_small);
         for (auto& e : ev) cudaEventDestroy(e);
@@ -534,6 +551,15 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.tile_cslot = ws.d_tile_cslot;
         f.cand_need = ws.d_small + 5;
         f.filter_k = dt.view.filter_k;
+        if (dt.sym_bits) {
+            const uint64_t per = 32 / dt.sym_bits, words = (n_avail + per - 1) / per;
+            ws.regrow(ws.d_packed, ws.packed_cap, words + 4);
+            CK(cudaMemsetAsync(ws.d_packed + words, 0, 4 * sizeof(uint32_t), ws.stream)); // overhang words
+            const unsigned blocks = unsigned(std::min<uint64_t>((words + 255) / 256, uint64_t(dt.sm_count) * 16));
+            dt.pack_fn<<<std::max(1u, blocks), 256, 0, ws.stream>>>(d_text, words, dt.view.symtab, ws.d_packed);
+            CK(cudaGetLastError());
+            f.packed = ws.d_packed;
+        }
         dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());
         if (between) CK(cudaEventRecord(between, ws.stream));
@@ -757,7 +783,7 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
-    li.filter_mode = d->kw == 0 ? 0u : ((d->pair && !d->lean_single) ? 2u : 1u);
+    li.filter_mode = d->kw == 0 ? 0u : (d->sym_bits ? 3u : ((d->pair && !d->lean_single) ? 2u : 1u));
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }

@@ -59,8 +59,9 @@ struct FilterArgs {
     uint32_t* tile_cslot;
     unsigned long long* cand_need; // max entries any warp needed (overflow sizing)
     // single-probe form (pfac_single_filter_kernel): k-byte key, table of
-    // table_words words (layout.hpp)
+    // table_words words (layout.hpp); symbol form: k symbols
     uint32_t filter_k;
+    const uint32_t* packed;  // symbol form: the text packed by pfac_pack_symbols_kernel
 };
 
 __device__ __forceinline__ uint32_t f_lds(uint32_t addr)
@@ -391,6 +392,122 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_single_filter_kernel(const 
         }
     }
     if (lane == 0 && cursor > a.cand_cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+}
+
+
+// ---- symbol-key form (small alphabets) ------------------------------------------
+
+// Packs the text to SB bits per symbol (byte -> alphabet symbol, bytes
+// outside the alphabet as symbol 0: only a filter input, the walks re-read
+// the bytes), one u32 per 32/SB bytes, LSB-first.
+template <int SB>
+__global__ void __launch_bounds__(256) pfac_pack_symbols_kernel(const uint8_t* __restrict__ text, uint64_t n_words,
+                                                               const uint16_t* __restrict__ symtab,
+                                                               uint32_t* __restrict__ packed)
+{
+    __shared__ uint32_t tab[256];
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+        const uint16_t v = symtab[i];
+        tab[i] = v == kNoSym ? 0u : v;
+    }
+    __syncthreads();
+    constexpr uint32_t per = 32 / SB; // bytes per packed word
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < n_words; w += uint64_t(gridDim.x) * blockDim.x) {
+        const uint8_t* src = text + w * per;
+        uint32_t bytes[per / 4];
+        if (per == 8) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+            bytes[0] = v.x, bytes[per / 4 - 1] = v.y;
+        } else {
+#pragma unroll
+            for (uint32_t q = 0; q < per / 16; ++q) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + q);
+                bytes[4 * q] = v.x, bytes[4 * q + 1] = v.y, bytes[4 * q + 2] = v.z, bytes[4 * q + 3] = v.w;
+            }
+        }
+        uint32_t key = 0;
+#pragma unroll
+        for (uint32_t i = 0; i < per; ++i) key |= tab[(bytes[i / 4] >> (8 * (i % 4))) & 0xFFu] << (SB * i);
+        packed[w] = key;
+    }
+}
+
+// Filter pass over packed symbols: lane L of a chunk owns packed word L (32/SB
+// starts); the key of start j is the SB*k bits from bit SB*j.  Survivors go to
+// the candidate regions with their packed key.
+template <int SB>
+__global__ void __launch_bounds__(kFThreads, 1) pfac_symbol_filter_kernel(const __grid_constant__ FilterArgs a)
+{
+    extern __shared__ __align__(128) uint8_t fsmem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
+    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
+    __syncthreads();
+    const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+    const uint32_t mask4 = (a.table_words - 1u) << 2;
+    const uint32_t kbits = SB * a.filter_k;
+    const uint32_t kmask = kbits >= 32 ? 0xFFFFFFFFu : ((1u << kbits) - 1u);
+    constexpr uint32_t kPer = 32 / SB;           // starts per packed word (lane)
+    constexpr uint32_t kChunk = 32 * kPer;       // starts per warp chunk
+    constexpr uint32_t kChunks = kFTile / kChunk;
+    const uint32_t* packed = a.packed;
+
+    const uint32_t gw = blockIdx.x * kFWarps + (tid >> 5), W = gridDim.x * kFWarps;
+    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
+    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
+    const uint32_t cap = uint32_t(min(a.cand_cap, uint64_t(0xFFFFFFFFu)));
+    uint32_t cursor = 0;
+    const uint32_t below = (1u << lane) - 1u;
+
+    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
+        const uint64_t lo = tile * kFTile;
+        const uint32_t slot = cursor;
+        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
+        const uint32_t chunks = (rem + kChunk - 1) / kChunk;
+        const uint64_t w0 = lo / kPer; // first packed word of the tile
+        for (uint32_t c = 0; c < chunks; ++c) {
+            const uint64_t wi = w0 + uint64_t(c) * 32 + lane;
+            const uint32_t a0 = __ldg(packed + wi), a1 = __ldg(packed + wi + 1); // padded array
+            uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < kPer; ++j) {
+                const uint32_t key = (j ? __funnelshift_r(a0, a1, SB * j) : a0) & kmask;
+                const uint32_t word = f_lds(tbase + (__umulhi(key, kFilterMul) & mask4)); // filter_word(key) * 4
+                uint32_t& m = j < kPer / 2 ? m0 : m1;
+                m = __funnelshift_l(__funnelshift_l(0u, word, key), m, 1);
+            }
+            // start j at bit j
+            uint32_t keep = __brev((m0 << (32 - kPer / 2)) | (kPer / 2 < 32 ? (m1 << (32 - kPer)) : 0u));
+            if (kPer < 32) keep &= (1u << kPer) - 1u;
+            const int32_t r = int32_t(rem) - int32_t(c * kChunk + kPer * lane);
+            keep &= r >= int32_t(kPer) ? 0xFFFFFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            if (!__any_sync(0xFFFFFFFFu, keep)) continue;
+            // survivors in start order (lane, j): a warp scan of the per-lane counts
+            const uint32_t n = __popc(keep);
+            uint32_t incl = n;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= uint32_t(d)) incl += u;
+            }
+            uint32_t at = cursor + incl - n;
+            const uint32_t first = c * kChunk + kPer * lane; // tile offset
+            for (uint32_t m = keep; m; m &= m - 1, ++at) {
+                const uint32_t j = __ffs(m) - 1;
+                if (at < cap) {
+                    region[at] = uint16_t(first + j);
+                    keys[at] = (j ? __funnelshift_r(a0, a1, SB * j) : a0) & kmask;
+                }
+            }
+            cursor += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        if (lane == 0) {
+            a.tile_ccount[tile] = cursor - slot;
+            a.tile_cslot[tile] = slot;
+        }
+    }
+    if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+    (void)kChunks;
 }
 
 } // namespace hfb::gpu

@@ -129,6 +129,8 @@ struct TrieView {
     uint32_t mul_shr16;   // IMAD.HI, balancing the filter's ALU (shift) and FMA pipes
     const uint32_t* filter2; // second level, 2^filter2_bits bits
     uint32_t filter2_bits;   // 0 = no second level
+    uint32_t sym_bits;       // symbol-key mode (small alphabets): bits per packed symbol (1, 2 or 4),
+                             // filter/jump keys are the first filter_k symbols packed LSB-first; 0 = byte keys
     const uint32_t* key4;    // pair pipeline: bitmap over the first 4 bytes of every depth-k path
     uint32_t key4_words;     // (single-probe hash, layout above); 0 = none
     const uint32_t* jump;    // 2^jump_bits uint4 slots

@@ -229,7 +229,11 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
     const TrieView& t = a.trie;
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
     const uint32_t limit = t.depth_limit ? t.depth_limit : 0xFFFFFFFFu;
-    uint32_t wpos = depth; // depth <= 8 here
+    uint32_t wpos = depth; // `win` holds text[start, start + 8)
+    if (depth > 8) {       // symbol-key jumps start deeper: the window of the current byte
+        win = (uint64_t(text_word(a, start + (depth & ~7u) + 4)) << 32) | text_word(a, start + (depth & ~7u));
+        wpos = depth & 7u;
+    }
     for (;;) {
         const bool more = depth < room;
         if (wpos == 8) { // next 8 bytes (the padded buffer makes the overread safe)
@@ -472,6 +476,41 @@ struct JumpHit {
     uint4 w;   // {lo, hi, node, term}
     uint4 aux; // {bk_first, bk_count, flags, 0}
 };
+__device__ __forceinline__ JumpHit jump_lookup_key(const TrieView& t, uint32_t lo, uint32_t hi)
+{
+    const uint32_t mask = (1u << t.jump_bits) - 1u;
+    const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
+    for (uint32_t s = jump_slot(lo ^ (hi * 0x85EBCA77u), t.jump_bits);; s = (s + 1) & mask) {
+        JumpHit h;
+        h.w = __ldg(slots + 2 * s);
+        h.aux = __ldg(slots + 2 * s + 1);
+        if (h.w.z == kNoId || (h.w.x == lo && h.w.y == hi)) return h;
+    }
+}
+
+// Symbol-key mode: the first filter_k symbols of the start, packed sym_bits
+// each (the host's key, image.cpp).  False when one of those bytes is outside
+// the alphabet: no trie path spells it (the packed filter input aliased it to
+// symbol 0, so this is where such starts are dropped).
+__device__ __forceinline__ bool symbol_key(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint32_t& key)
+{
+    const TrieView& t = a.trie;
+    const uint32_t k = t.filter_k, sb = t.sym_bits;
+    bool ok = true;
+    key = 0;
+    for (uint32_t i = 0; i < k; i += 4) {
+        const uint32_t w = text_word(a, start + i);
+#pragma unroll
+        for (uint32_t b = 0; b < 4; ++b)
+            if (i + b < k) {
+                const uint32_t s = s_sym[(w >> (8 * b)) & 0xFFu];
+                ok = ok && s != kNoSym;
+                key |= (s == kNoSym ? 0u : s) << (sb * (i + b));
+            }
+    }
+    return ok;
+}
+
 template <int KW>
 __device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
 {
@@ -555,7 +594,13 @@ struct Walker {
                 start = lo + q[e];
                 win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
                 if (KW != 0 && a.trie.jump_bits) {
-                    hit = jump_lookup<KW>(a.trie, win);
+                    if (a.trie.sym_bits) {
+                        uint32_t key;
+                        if (symbol_key(a, s_sym, start, key)) hit = jump_lookup_key(a.trie, key, 0u);
+                        else hit.w.z = kNoId;
+                    } else {
+                        hit = jump_lookup<KW>(a.trie, win);
+                    }
                     node = hit.w.z;
                     depth = a.trie.filter_k;
                 }
@@ -736,10 +781,13 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                         const uint64_t t_i = unit * kSuper + i;
                         const uint64_t at = (t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i);
                         v = uint16_t(a.cand[at] + i * kTile);
-                        const uint32_t key = a.cand_key[at];
-                        const uint32_t word =
-                            *reinterpret_cast<const uint32_t*>(kbytes + (__umulhi(key, kFilterMul) & kmask4));
-                        keep = fwords == 0 || int32_t(word << (key & 31u)) < 0;
+                        keep = true;
+                        if (fwords) { // no prefix bitmap in symbol-key mode
+                            const uint32_t key = a.cand_key[at];
+                            const uint32_t word =
+                                *reinterpret_cast<const uint32_t*>(kbytes + (__umulhi(key, kFilterMul) & kmask4));
+                            keep = int32_t(word << (key & 31u)) < 0;
+                        }
                     }
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
                     if (keep) wk.q[kept + __popc(bal & ((1u << lane) - 1u))] = v;

@@ -44,6 +44,7 @@ ImageOptions image_options_from_env()
     }
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_LEAN_SINGLE")) o.lean_single = std::strtol(s, nullptr, 10) != 0;
+    if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
         const std::string m = s;
         o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : 0u);
@@ -429,6 +430,84 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     uint32_t* slot = &im.jump[W * s];
                     slot[0] = uint32_t(grams[i]);
                     slot[1] = uint32_t(grams[i] >> 32);
+                    slot[2] = node;
+                    slot[3] = im.term_id[node];
+                    const uint32_t b = im.bucket_of[node];
+                    slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
+                    slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
+                    slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
+                }
+            }
+        }
+    }
+    // ---- symbol-key mode (small alphabets) -----------------------------------
+    // Byte keys carry log2(sigma) bits per byte: 8 bytes of DNA are 16 bits, of
+    // a binary alphabet 8.  When the shortest report depth allows more than 8
+    // symbols, keys are the first k symbols packed at 1/2/4 bits each, up to
+    // 32 bits: sigma = 4 with 12-symbol keys has 24 bits of selectivity.  The
+    // text is packed once per scan (pfac_pack_symbols_kernel) and scanned by
+    // the symbol filter pass; the jump table is keyed the same way.
+    {
+        const uint32_t sigma = t.alphabet.size();
+        // 4-bit symbols would need more than 8 of them (> 32-bit keys) to beat
+        // byte keys, so symbol keys serve sigma <= 4
+        const uint32_t sb = sigma <= 2 ? 1u : (sigma <= 4 ? 2u : 0u);
+        const uint32_t ks = sb && im.min_emit != UINT32_MAX ? std::min(im.min_emit, 32u / sb) : 0u;
+        if (opt.symbol_keys && sb && ks > std::min(im.min_emit, kMaxFilterKey) && opt.jump) {
+            std::vector<uint32_t> keys, knode;
+            struct SFrame {
+                uint32_t node, depth, key;
+            };
+            std::vector<SFrame> st{{0u, 0u, 0u}};
+            bool overflow = false;
+            while (!st.empty() && !overflow) {
+                const SFrame f = st.back();
+                st.pop_back();
+                if (f.depth == ks) {
+                    keys.push_back(f.key);
+                    knode.push_back(f.node);
+                    overflow = keys.size() > (uint64_t(1) << 22);
+                    continue;
+                }
+                const uint32_t* c = t.cell(f.node);
+                uint32_t child = t.offset(f.node);
+                for (uint32_t w = 0; w < t.words; ++w)
+                    for (uint32_t bits = c[w]; bits; bits &= bits - 1) {
+                        const uint32_t s = w * 32 + uint32_t(__builtin_ctz(bits));
+                        st.push_back({child++, f.depth + 1, f.key | (s << (sb * f.depth))});
+                    }
+            }
+            if (!overflow && !keys.empty()) {
+                im.filter_mode = 3;
+                im.sym_bits = sb;
+                im.filter_k = ks;
+                im.filter_paths = keys.size();
+                const uint32_t bits =
+                    std::clamp<uint32_t>(ceil_log2(keys.size()) + opt.filter_slack, 10, opt.max_filter_bits);
+                im.filter_bits = bits;
+                im.filter.assign((size_t(1) << bits) / 32, 0u);
+                for (uint32_t key : keys) im.filter[filter_word(key, bits - 5)] |= filter_mask_bit(key);
+                // fraction of uniform random texts that survive: fill of the bitmap
+                uint64_t set = 0;
+                for (uint32_t w : im.filter) set += uint64_t(__builtin_popcount(w));
+                im.filter_pass = double(set) / double(uint64_t(1) << bits);
+                im.filter2_bits = 0;
+                im.filter2.clear();
+                im.key4.clear();
+                im.lean_single = false;
+                const uint32_t jb = std::max<uint32_t>(ceil_log2(keys.size()) + 1, 4);
+                const uint32_t mask = (1u << jb) - 1u;
+                constexpr size_t W = kJumpWords;
+                im.jump_bits = jb;
+                im.jump.assign(W << jb, 0u);
+                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[W * s + 2] = kNoId;
+                for (size_t i = 0; i < keys.size(); ++i) {
+                    uint32_t s = jump_slot(keys[i], jb); // filter_fold(key) == key for 32-bit keys
+                    while (im.jump[W * s + 2] != kNoId) s = (s + 1) & mask;
+                    const uint32_t node = knode[i];
+                    uint32_t* slot = &im.jump[W * s];
+                    slot[0] = keys[i];
+                    slot[1] = 0;
                     slot[2] = node;
                     slot[3] = im.term_id[node];
                     const uint32_t b = im.bucket_of[node];

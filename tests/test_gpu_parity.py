@@ -352,3 +352,42 @@ def test_lean_single_pipeline(gpu, monkeypatch, stages, depth):
     for i, p in enumerate(pats):
         plant(tx, p, (i * 331) % (tx.size - 24))
     assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
+
+
+@pytest.mark.parametrize("sigma", [2, 4])
+def test_symbol_key_mode(gpu, sigma):
+    # small alphabets with long shortest patterns: filter and jump keys are
+    # packed symbols (filter_mode 3) -- every trie state, text sizes around the
+    # packed-word and tile boundaries, bytes outside the alphabet
+    rng = np.random.default_rng(50 + sigma)
+    a, syms = alphabet_bytes(gpu, sigma)
+    pats = pattern_set(rng, syms, 400, 10, 24)
+    full = build(gpu, pats, sigma)
+    assert gpu.layout_info(full)["filter_mode"] == 3
+    s1, _ = full.compress(1)
+    s2, _ = full.compress(2)
+    tries = [full, s1, s2] + [tr for tr, noop in (s1.truncate(d) for d in (10, 12, 16)) if not noop]
+    for n in (1, 9, 31, 33, 8191, 8193, 70001):
+        tx = text(rng, syms, n)
+        for i in range(0, max(1, n - 30), 97):
+            plant(tx, pats[i % len(pats)], i)
+        if n > 100:
+            tx[50] = 0xFF  # outside every standard alphabet
+            tx[n // 2] = 0x00
+        want = oracle.naive_find_all(tx, pats)
+        for t in tries:
+            assert same(gpu.scan(t, tx), want), (sigma, n, t.stage(), t.depth_limit())
+
+
+def test_symbol_key_mode_streamed(gpu, monkeypatch):
+    rng = np.random.default_rng(77)
+    a, syms = alphabet_bytes(gpu, 4)
+    pats = pattern_set(rng, syms, 300, 12, 30)
+    t, _ = build(gpu, pats, 4).compress(1)
+    t, _ = t.truncate(12)
+    tx = text(rng, syms, 3 * (1 << 20) + 777)
+    for c in range(1 << 20, tx.size, 1 << 20):
+        p = pats[c % len(pats)]
+        plant(tx, p, c - len(p) // 2)
+    monkeypatch.setenv("HEPFAC_CHUNK_MIB", "1")
+    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
