@@ -243,9 +243,6 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter_k = im.filter_k;
     v.sym_bits = im.sym_bits;
     v.pair_shift = im.pair_shift;
-    v.pair_mul = im.pair_shift ? 1u << (32 - im.pair_shift) : 0u;
-    v.mul_shr8 = 1u << 24;
-    v.mul_shr16 = 1u << 16;
     v.filter2 = d->upload(im.filter2);
     v.key4 = d->upload(im.key4.empty() ? std::vector<uint32_t>(1, 0u) : im.key4);
     v.key4_words = uint32_t(im.key4.size());

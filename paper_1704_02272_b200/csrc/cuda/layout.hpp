@@ -124,9 +124,6 @@ struct TrieView {
     uint32_t filter_bits; // 0 = filter disabled (every start walks)
     uint32_t filter_k;
     uint32_t pair_shift;  // pair form: 32 - log2(words), i.e. word = (middle * kPairMul) >> pair_shift
-    uint32_t pair_mul;    // 1 << log2(words): the same shift as a high multiply (FMA pipe, not ALU)
-    uint32_t mul_shr8;    // 1 << 24 and 1 << 16, opaque to the compiler: x >> 8 and x >> 16 as
-    uint32_t mul_shr16;   // IMAD.HI, balancing the filter's ALU (shift) and FMA pipes
     const uint32_t* filter2; // second level, 2^filter2_bits bits
     uint32_t filter2_bits;   // 0 = no second level
     uint32_t sym_bits;       // symbol-key mode (small alphabets): bits per packed symbol (1, 2 or 4),

@@ -1,28 +1,35 @@
-// scan_kernel.cuh -- the sm_100a PFAC match kernel.
+// scan_kernel.cuh -- the sm_100a PFAC match kernels: the one-pass scan and
+// the candidate-walking pass of the two-pass pipeline (filter_kernel.cuh has
+// the filter passes).
 //
 // Reference semantics: scan.cpp:20-51 (walk), :69-119 (scan), trie.hpp:68-79
 // (transition).  One logical walk per text offset, as in the paper
 // (PAPER.md:87-95).
 //
-// GPU work decomposition: one cooperative, persistent launch with one CTA per
-// SM.  Block-wide state is read-only: the start filter (a bitmap over the
-// trie's depth-k path strings) and the byte->symbol map, in shared memory.
-// Everything else is per warp, so no warp ever waits for another during the
-// scan itself:
+// pfac_scan_kernel<GROUPED, IDENT, KW, PAIR, CANDS>: one cooperative,
+// persistent launch with one CTA per SM.
 //
+// CANDS = false (one-pass).  Block-wide state is read-only: the start filter
+// and the byte->symbol map in shared memory.  Everything else is per warp:
 //   phase 1, per warp, over statically interleaved 8 KiB warp-tiles
-//   (8 groups of 1 KiB: 32 lanes x 32 consecutive starts):
+//   (8 groups of 1 KiB; each lane owns two 16-start slices per group):
 //     - lane 0 keeps kStages groups in flight with cp.async.bulk (TMA bulk
 //       copies, mbarrier-tracked) into the warp's ring in shared memory;
-//     - each lane probes the filter for its 32 starts (7 SASS instructions per
-//       start: one shared-memory word load, one funnel shift to test the bit);
+//     - each lane reads its two slices (conflict-free 16-byte loads; the
+//       overhang from the next lane by SHFL) and probes the start filter:
+//       single probe per start, or pair probes (one per two starts) plus the
+//       in-lane second role test;
 //     - survivors are compacted in start order into a per-warp queue and
-//       walked right away, lane-parallel, reading text from the staged group
-//       (the trie image through __ldg: one 8/16-byte record per text byte);
+//       walked 32 at a time (Walker::flush): depth-k jump table, one node
+//       record per text byte, bucket verification at the depth limit;
 //     - a warp scan of the per-lane record counts appends the records, in
 //       order, to the warp's private staging region in HBM; per tile the
 //       record count and staging offset go to a small table.
-//   grid sync -> phase 2: per-CTA sums of the tile counts.
+// CANDS = true (walking pass): phase 1 takes units of kSuper tiles from an
+//   atomic counter, loads their candidates (left by the filter pass), drops
+//   those whose 4-byte prefix misses a shared-memory bitmap, and walks the
+//   rest with the same Walker.
+// Both: grid sync -> phase 2: per-CTA sums of the tile counts.
 //   grid sync -> phase 3: each CTA scans its contiguous range of tiles and
 //     copies their staged records to their final offsets, so the output is
 //     in (start, length, id) order without a sort (the reference merges per
@@ -321,68 +328,43 @@ __device__ __forceinline__ uint32_t table_word(uint32_t off)
     return v;
 }
 
-// Pair form (layout.hpp): 16 probes for the lane's 32 starts.  Probe p reads
-// the word of the middle at odd position i = 2p + 1 and tests start i - 1
-// (role A: bit of its first byte) and start i (role B: bit of its 4th byte).
-// Returns bit j = start j passed its first role.
-#ifndef HFB_CHAINS
-#define HFB_CHAINS 4 // independent mask accumulators in the pair filter
-#endif
-#ifndef HFB_HASHHI
-#define HFB_HASHHI 0 // pair hash shift as IMAD.HI (FMA pipe) instead of SHF (ALU pipe)
-#endif
-#ifndef HFB_WINHI
-#define HFB_WINHI 0 // in-word windows as IMAD.HI instead of funnel shifts
-#endif
-
+// Pair form (layout.hpp): 8 probes for a 16-start slice.  Probe p reads the
+// word of the middle at odd position i = 2p + 1 and tests start i - 1 (role A:
+// bit of its first byte) and start i (role B: bit of its 4th byte).
+// filter_pair returns bit j = start j passed its first role.
 __device__ __forceinline__ uint32_t pair_offset(const TrieView& t, uint32_t mid)
 {
-    const uint32_t h = mid * kPairMul;
-    return (HFB_HASHHI ? __umulhi(h, t.pair_mul) : (h >> t.pair_shift)) << 2; // pair_word(mid) * 4
+    return ((mid * kPairMul) >> t.pair_shift) << 2; // pair_word(mid) * 4
 }
 
 __device__ __forceinline__ uint32_t filter_pair(const TrieView& t, const uint32_t (&w)[5], uint32_t valid)
 {
-    // Windows at 4q+1 (x >> 8) and 4q+2 (x >> 16) may come off the FMA pipe
-    // as high multiplies; those spanning two words are ALU funnel shifts.
     // Only the low 24 bits of a middle and the low 5 of an amount matter.
     auto window = [&](int n) -> uint32_t {
         switch (n & 3) {
         case 0: return w[n >> 2];
-        case 1: return HFB_WINHI ? __umulhi(w[n >> 2], t.mul_shr8) : (w[n >> 2] >> 8);
-        case 2: return HFB_WINHI ? __umulhi(w[n >> 2], t.mul_shr16) : (w[n >> 2] >> 16);
+        case 1: return w[n >> 2] >> 8;
+        case 2: return w[n >> 2] >> 16;
         default: return __funnelshift_r(w[n >> 2], w[(n >> 2) + 1], 24);
         }
     };
-    // independent accumulators keep the dependent funnel-shift chains short
-    constexpr int kChains = HFB_CHAINS > 2 ? 2 : HFB_CHAINS;
-    constexpr int kPer = int(kSliceStarts) / kChains;
-    uint32_t m[kChains];
-#pragma unroll
-    for (int c = 0; c < kChains; ++c) m[c] = 0u;
+    uint32_t m0 = 0, m1 = 0; // two independent accumulator chains, MSB-first
 #pragma unroll
     for (int i = 1; i < int(kSliceStarts); i += 2) {
         const uint32_t mid = window(i);
         const uint32_t amt_a = window(i - 1), amt_b = window(i + 3);
         const uint32_t word = table_word(pair_offset(t, mid));
-        uint32_t& acc = m[i / kPer];
+        uint32_t& acc = i < 8 ? m0 : m1;
         acc = __funnelshift_l(__funnelshift_l(0u, word, amt_a), acc, 1); // start i - 1
         acc = __funnelshift_l(__funnelshift_l(0u, word, amt_b), acc, 1); // start i
     }
-    uint32_t msb_first = 0; // start j at bit 31 - j
-#pragma unroll
-    for (int c = 0; c < kChains; ++c) msb_first |= m[c] << (32 - kPer * (c + 1));
-    return __brev(msb_first) & valid;
+    return __brev((m0 << 24) | (m1 << 16)) & valid; // start j at bit j
 }
 
 // Second pair level: each survivor j of `mask` tests its other role (odd j:
 // role A at the middle j + 1; even j: role B at the middle j), reading its 4
 // bytes back from the staged lane slice `src` in shared memory.  Two
 // survivors (the lowest and the highest) per round for latency overlap.
-#ifndef HFB_L2PAIR
-#define HFB_L2PAIR 1 // second level handles two survivors per round
-#endif
-
 __device__ __forceinline__ bool pair_second_test(const TrieView& t, const uint8_t* src, uint32_t j)
 {
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(src + (j & ~3u));
@@ -397,20 +379,13 @@ __device__ __forceinline__ bool pair_second_test(const TrieView& t, const uint8_
 __device__ __forceinline__ uint32_t filter_pair_second(const TrieView& t, uint32_t mask, const uint8_t* src)
 {
     uint32_t keep = mask;
-    if (HFB_L2PAIR) {
-        for (uint32_t c = mask; c;) {
-            const uint32_t lo = __ffs(c) - 1, hi = 31 - __clz(c);
-            c &= ~((1u << lo) | (1u << hi));
-            const bool ok_lo = pair_second_test(t, src, lo);
-            const bool ok_hi = pair_second_test(t, src, hi);
-            if (!ok_lo) keep &= ~(1u << lo);
-            if (!ok_hi) keep &= ~(1u << hi);
-        }
-    } else {
-        for (uint32_t c = mask; c; c &= c - 1) {
-            const uint32_t j = __ffs(c) - 1;
-            if (!pair_second_test(t, src, j)) keep &= ~(1u << j);
-        }
+    for (uint32_t c = mask; c;) { // the lowest and the highest survivor per round
+        const uint32_t lo = __ffs(c) - 1, hi = 31 - __clz(c);
+        c &= ~((1u << lo) | (1u << hi));
+        const bool ok_lo = pair_second_test(t, src, lo);
+        const bool ok_hi = pair_second_test(t, src, hi);
+        if (!ok_lo) keep &= ~(1u << lo);
+        if (!ok_hi) keep &= ~(1u << hi);
     }
     return keep;
 }
@@ -554,14 +529,7 @@ struct Walker {
 
     // Candidates [0, n) of the tile starting at `lo`: second-level probe,
     // then walk the survivors and append their records in start order.
-#ifndef HFB_FLUSH_NOINLINE
-#define HFB_FLUSH_NOINLINE 0
-#endif
-#if HFB_FLUSH_NOINLINE
-    __device__ __noinline__ void flush(uint64_t lo, uint32_t n)
-#else
     __device__ __forceinline__ void flush(uint64_t lo, uint32_t n)
-#endif
     {
         uint32_t ns = n;
         if (KW != 0 && a.trie.filter2_bits) {
