@@ -391,3 +391,38 @@ def test_symbol_key_mode_streamed(gpu, monkeypatch):
         plant(tx, p, c - len(p) // 2)
     monkeypatch.setenv("HEPFAC_CHUNK_MIB", "1")
     assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
+
+
+def test_config3_full_size_against_reference(gpu, ref):
+    # BASELINE config 3 at its bench size per GPU (4 GiB of text, 20k
+    # signatures, the benchmark trie), device-resident through the two-pass
+    # pipeline and through the streamed hepfac_scan path, against the
+    # compiled reference on all host threads: identical arrays.  Offsets past
+    # 2^32 are exercised by a 4.5 GiB text.
+    from paper_1704_02272_b200 import workloads
+    w = workloads.config("c3")
+    tx = w.make_text((4 << 30) + (512 << 20))
+    t, _ = workloads.build_trie(gpu, w, "s1trunc")
+    rt, _ = workloads.build_trie(ref, w, "s1trunc")
+    want = ref.scan(rt, tx, workers=os.cpu_count())
+    s = gpu.session(t, tx)
+    s.run(1)
+    assert s.kernel_ms(1)[2] == 2
+    assert same(s.fetch(), want)
+    s.close()
+    assert same(gpu.scan(t, tx), want)
+    assert want.size > 1_000_000 and int(want["start"][-1]) >= (1 << 32)
+
+
+@pytest.mark.parametrize("state", ["s1trunc", "stage2"])
+def test_config2_full_size_against_reference(gpu, ref, state):
+    # BASELINE config 2 at full size: DNA, 10k patterns len 8-32, 1 GiB genome
+    # (8.3 M matches), identical to the compiled reference.
+    from paper_1704_02272_b200 import workloads
+    w = workloads.config("c2")
+    tx = w.make_text(1 << 30)
+    t, _ = workloads.build_trie(gpu, w, state)
+    rt, _ = workloads.build_trie(ref, w, state)
+    want = ref.scan(rt, tx, workers=os.cpu_count())
+    assert want.size > 8_000_000
+    assert same(gpu.scan(t, tx), want)
