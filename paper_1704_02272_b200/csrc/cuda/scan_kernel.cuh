@@ -129,20 +129,55 @@ __device__ __noinline__ bool same_bytes(const ScanArgs& a, uint64_t start, uint3
     return true;
 }
 
+__device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint64_t off, uint32_t len);
+
 // Shared terminal: identify the slice by its key, then confirm it (the
 // reference's dictionary lookup, trie.hpp:103-107; a miss is its logic_error
 // "terminal node spells no dictionary pattern", scan.cpp:34).
+// PAR (the walking pass, where stage-2 matches resolve often): every load of
+// a stage is issued before its first use -- the slice's words 32 bytes at a
+// time, a probe's id and key together, the pattern's length and offset
+// together.  The one-pass kernel keeps the compact sequential form (measured:
+// the parallel one costs its register allocation 11% at c2).
+template <bool PAR>
 __device__ __noinline__ uint32_t resolve_slice(const ScanArgs& a, uint64_t start, uint32_t len)
 {
     const TrieView& t = a.trie;
     uint64_t h = 0;
-    for (uint32_t i = 0; i < len; i += 4) h = slice_step(h, t.hmul, text_word(a, start + i) & tail_mask(len - i));
+    if (PAR) {
+        const uint32_t sh = uint32_t(start & 3u) * 8u;
+        for (uint32_t i = 0; i < len; i += 32) {
+            const uint32_t* tw = reinterpret_cast<const uint32_t*>(a.text + ((start + i) & ~3ull));
+            const uint32_t nw = min(8u, (len - i + 3) / 4);
+            uint32_t tx[9];
+#pragma unroll
+            for (uint32_t k = 0; k < 9; ++k) tx[k] = k <= nw ? __ldg(tw + k) : 0u; // padded text
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k)
+                if (k < nw) {
+                    const uint32_t w = sh ? __funnelshift_r(tx[k], tx[k + 1], sh) : tx[k];
+                    h = slice_step(h, t.hmul, w & tail_mask(len - i - 4 * k));
+                }
+        }
+    } else {
+        for (uint32_t i = 0; i < len; i += 4) h = slice_step(h, t.hmul, text_word(a, start + i) & tail_mask(len - i));
+    }
     const uint64_t key = slice_key(h, len);
     for (uint64_t s = mix64(key) & t.ht_mask;; s = (s + 1) & t.ht_mask) {
         const uint32_t id = __ldg(t.ht_id + s);
-        if (id == kNoId) return kNoId;
-        if (__ldg(t.ht_key + s) == key)
-            return (__ldg(t.pat_len + id) == len && same_bytes(a, start, id, len)) ? id : kNoId;
+        if (PAR) {
+            const uint64_t k2 = __ldg(t.ht_key + s);
+            if (id == kNoId) return kNoId;
+            if (k2 == key) {
+                const uint32_t plen = __ldg(t.pat_len + id);
+                const uint64_t poff = __ldg(t.pat_off + id);
+                return (plen == len && same_at(a, start, poff, len)) ? id : kNoId;
+            }
+        } else {
+            if (id == kNoId) return kNoId;
+            if (__ldg(t.ht_key + s) == key)
+                return (__ldg(t.pat_len + id) == len && same_bytes(a, start, id, len)) ? id : kNoId;
+        }
     }
 }
 
@@ -229,7 +264,7 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 //
 // A walk may begin below the root: (node, depth) from the jump table, which
 // is only used for depth <= min_emit, where nothing above can report.
-template <bool GROUPED, bool IDENT>
+template <bool GROUPED, bool IDENT, bool PAR>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
                                      uint32_t node, uint32_t depth, Sink& sink)
 {
@@ -267,7 +302,7 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
         }
         if (depth && (meta & kFlagTerminal)) {
             uint32_t id = GROUPED ? inline_id : __ldg(t.term_id + node);
-            if (id == kNoId) id = resolve_slice(a, start, depth);
+            if (id == kNoId) id = resolve_slice<PAR>(a, start, depth);
             if (id == kNoId) atomicOr(a.err, 1u);
             else sink.put(a.g0 + start, depth, id);
         }
@@ -506,19 +541,20 @@ __device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
 // A walk that starts at the depth limit (k == limit): the node's terminal
 // record and its bucket come from the jump slot (walk() semantics at the
 // limit: terminal first, then the bucket in (length, id) order).
+template <bool PAR>
 __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& h, uint64_t start, uint32_t depth,
                                               Sink& sink)
 {
     if (h.aux.z & 1u) {
         uint32_t id = h.w.w;
-        if (id == kNoId) id = resolve_slice(a, start, depth);
+        if (id == kNoId) id = resolve_slice<PAR>(a, start, depth);
         if (id == kNoId) atomicOr(a.err, 1u);
         else sink.put(a.g0 + start, depth, id);
     }
     if (h.aux.z & 2u) verify_span(a, make_uint2(h.aux.x, h.aux.y), start, sink);
 }
 
-template <bool GROUPED, bool IDENT, int KW>
+template <bool GROUPED, bool IDENT, int KW, bool PAR>
 struct Walker {
     const ScanArgs& a;
     const uint16_t* s_sym;
@@ -573,8 +609,8 @@ struct Walker {
                     depth = a.trie.filter_k;
                 }
                 if (node != kNoId) {
-                    if (at_limit) emit_at_limit(a, hit, start, depth, sink);
-                    else walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, sink);
+                    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
+                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink);
                 }
             }
             uint32_t tot;
@@ -590,8 +626,8 @@ struct Walker {
                     wr.at = at + kRegRecords;
                     wr.cap = a.warp_cap;
                     wr.skip = kRegRecords;
-                    if (at_limit) emit_at_limit(a, hit, start, depth, wr);
-                    else walk<GROUPED, IDENT>(a, s_sym, start, win, node, depth, wr);
+                    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
+                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr);
                 }
             }
             cursor += tot;
@@ -693,7 +729,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
     }
     __syncthreads(); // filter, symbol map and barrier inits visible
 
-    Walker<GROUPED, IDENT, KW> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
+    Walker<GROUPED, IDENT, KW, CANDS> wk{a, s_sym, s_queue + warp * kQueue, lane, a.stage + uint64_t(gw) * a.warp_cap, 0};
     if constexpr (CANDS) {
         // Walk units of kSuper filter tiles: lane i < kSuper fetches tile i's
         // candidate count and slot, so one load latency covers the unit, and
