@@ -10,7 +10,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <exception>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../host/image.hpp"
 #include "engine.hpp"
@@ -693,7 +696,7 @@ uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, u
 // go to the device in one piece; longer ones are streamed chunk by chunk so
 // the H2D copy overlaps the kernels.
 std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,
-                                         uint64_t g0)
+                                         uint64_t g0, int device = -1)
 {
     auto out = std::make_unique<MatchList>();
     ScanStats st;
@@ -702,7 +705,7 @@ std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uin
         t_stats = st;
         return out;
     }
-    const int dev = pick_device();
+    const int dev = device >= 0 ? device : pick_device();
     st.device = dev;
     DeviceGuard g(dev);
     auto dt = t.device_image(dev);
@@ -741,9 +744,86 @@ std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uin
 
 const ScanStats& last_scan_stats() { return t_stats; }
 
+// HEPFAC_DEVICES: devices one hepfac_scan call shards its text over
+// ("all", or a comma list such as "0,1,2,3"; a device may repeat).  Unset:
+// the single device of pick_device().
+std::vector<int> scan_devices()
+{
+    const char* s = std::getenv("HEPFAC_DEVICES");
+    if (!s || !*s) return {pick_device()};
+    const int n = device_count();
+    if (n <= 0) pick_device(); // fails with the no-device message
+    std::vector<int> devs;
+    if (std::string(s) == "all") {
+        for (int d = 0; d < n; ++d) devs.push_back(d);
+        return devs;
+    }
+    for (const char* p = s; *p;) {
+        char* end = nullptr;
+        const long d = std::strtol(p, &end, 10);
+        if (end == p || d < 0 || d >= n) invalid("HEPFAC_DEVICES lists an invalid device");
+        devs.push_back(int(d));
+        p = *end == ',' ? end + 1 : end;
+        if (*end && *end != ',') invalid("HEPFAC_DEVICES must be 'all' or a comma-separated device list");
+    }
+    if (devs.empty()) invalid("HEPFAC_DEVICES lists no device");
+    return devs;
+}
+
+// Multi-GPU hepfac_scan: contiguous shards of starts, each with
+// the halo its walks may read, scanned concurrently (one host thread per
+// shard); the shards' sorted lists concatenate in shard order, which is the
+// whole list's order -- the exclusive scan of per-shard counts is the host's
+// output offset of each shard.
 std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t bytes)
 {
-    return scan_resident(t, text, bytes, bytes, 0);
+    const std::vector<int> devs = scan_devices();
+    constexpr uint64_t kMinShard = uint64_t(16) << 20;
+    const uint64_t G = std::min<uint64_t>(devs.size(), std::max<uint64_t>(1, bytes / kMinShard));
+    if (G <= 1) return scan_resident(t, text, bytes, bytes, 0, devs[0]);
+    const uint64_t reach = t.device_image(devs[0])->reach;
+    if (reach == UINT64_MAX) return scan_resident(t, text, bytes, bytes, 0, devs[0]); // cyclic: no halo bound
+    const uint64_t halo = reach ? reach - 1 : 0;
+    std::vector<std::unique_ptr<MatchList>> parts(G);
+    std::vector<ScanStats> stats(G);
+    std::vector<std::exception_ptr> errs(G);
+    std::vector<std::thread> pool;
+    for (uint64_t g = 0; g < G; ++g)
+        pool.emplace_back([&, g] {
+            try {
+                const uint64_t lo = bytes * g / G, hi = bytes * (g + 1) / G;
+                const uint64_t avail = std::min(bytes - lo, hi - lo + halo);
+                parts[g] = scan_resident(t, text + lo, avail, hi - lo, lo, devs[g]);
+                stats[g] = t_stats;
+            } catch (...) {
+                errs[g] = std::current_exception();
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    auto out = std::make_unique<MatchList>();
+    uint64_t total = 0;
+    for (auto& p : parts) total += p->size;
+    out->allocate(size_t(total));
+    ScanStats st;
+    st.bytes = bytes;
+    st.device = devs[0];
+    uint64_t at = 0;
+    for (uint64_t g = 0; g < G; ++g) {
+        if (parts[g]->size) std::memcpy(out->data + at, parts[g]->data, parts[g]->size * sizeof(hepfac_match_t));
+        at += parts[g]->size;
+        st.kernel_launches += stats[g].kernel_launches;
+        st.chunks += stats[g].chunks;
+        st.relaunches += stats[g].relaunches;
+        st.h2d_ms = std::max(st.h2d_ms, stats[g].h2d_ms);
+        st.kernel_ms = std::max(st.kernel_ms, stats[g].kernel_ms);
+        st.d2h_ms = std::max(st.d2h_ms, stats[g].d2h_ms);
+        st.total_ms = std::max(st.total_ms, stats[g].total_ms);
+    }
+    st.matches = total;
+    t_stats = st;
+    return out;
 }
 
 std::unique_ptr<MatchList> gpu_scan_shard(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,

@@ -426,3 +426,29 @@ def test_config2_full_size_against_reference(gpu, ref, state):
     want = ref.scan(rt, tx, workers=os.cpu_count())
     assert want.size > 8_000_000
     assert same(gpu.scan(t, tx), want)
+
+
+@pytest.mark.parametrize("devices", ["0,0,0", "all", "0,0"])
+def test_multi_device_scan(gpu, monkeypatch, devices):
+    # HEPFAC_DEVICES: one hepfac_scan shards its text into contiguous start
+    # ranges with halos, one host thread per shard (a device may repeat, so a
+    # one-GPU box exercises the sharded path), lists concatenated in order.
+    rng = np.random.default_rng(61)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 800, 3, 40)
+    tx = text(rng, syms, 50 * (1 << 20) + 4321)
+    for i in range(0, tx.size - 64, 65537):
+        plant(tx, pats[i % len(pats)], i)
+    for g in range(1, 4):  # straddle the shard seams of 2 and 3 shards
+        for c in (tx.size * g // 3, tx.size * g // 2):
+            p = pats[(c + g) % len(pats)]
+            plant(tx, p, c - len(p) // 2)
+    t = build(gpu, pats, 256, 2)
+    want = gpu.scan(t, tx)
+    monkeypatch.setenv("HEPFAC_DEVICES", devices)
+    got = gpu.scan(t, tx)
+    assert same(got, want)
+    from paper_1704_02272_b200 import hepfac as H
+    monkeypatch.setenv("HEPFAC_DEVICES", "9")
+    with pytest.raises(H.HepfacError):
+        gpu.scan(t, tx)
