@@ -228,6 +228,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.nodes = d->upload(im.nodes);
     v.term_id = d->upload(im.term_id);
     v.bucket_of = d->upload(im.bucket_of);
+    v.path_id = d->upload(im.path_id);
     v.groups = im.groups;
     v.depth_limit = im.depth_limit;
     v.symtab = d->upload(std::vector<uint16_t>(im.symtab.begin(), im.symtab.end()));
@@ -777,6 +778,7 @@ std::vector<int> scan_devices()
 // output offset of each shard.
 std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t bytes)
 {
+    if (bytes == 0) return scan_resident(t, text, 0, 0, 0); // empty: never touches a device
     const std::vector<int> devs = scan_devices();
     constexpr uint64_t kMinShard = uint64_t(16) << 20;
     const uint64_t G = std::min<uint64_t>(devs.size(), std::max<uint64_t>(1, bytes / kMinShard));

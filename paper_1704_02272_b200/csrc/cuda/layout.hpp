@@ -28,6 +28,7 @@ constexpr uint32_t kFlagBucket = 0x40000000u;
 constexpr uint32_t kBaseMask = 0x3FFFFFFFu;
 constexpr uint32_t kMaxGpuNodes = 0x40000000u;
 constexpr uint32_t kNoId = 0xFFFFFFFFu;
+constexpr uint32_t kKeep = 0xFFFFFFFEu; // path_id of a node that does not change the walk's path id
 constexpr uint16_t kNoSym = 0xFFFFu;
 constexpr uint32_t kMaxFilterKey = 8; // bytes hashed by the start filter
 
@@ -94,11 +95,12 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 // {lo, hi}) -> the node it reaches.  No node above depth k can report
 // (k <= min_emit), so a walk may start there instead of at the root.  Open
 // addressing, load <= 1/2, 32-byte slots
-//   {lo, hi, node, term, bk_first, bk_count, flags, 0}
+//   {lo, hi, node, term, bk_first, bk_count, flags, pend}
 // node == kNoId marks an empty slot.  The rest describes the node itself, so a
 // walk that starts at the depth limit (truncated tries with k == limit) emits
 // without reading the node record or the bucket index: term = its private
-// pattern id (kNoId = resolve by key), flags bit 0 terminal, bit 1 bucket.
+// pattern id (kNoId = resolve by key), flags bit 0 terminal, bit 1 bucket,
+// pend = the path id a walk carries at the node (image.cpp "path ids").
 constexpr uint32_t kJumpWords = 8;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 
@@ -107,6 +109,7 @@ struct TrieView {
     const uint32_t* nodes;
     const uint32_t* term_id;   // per node: private pattern id, or kNoId = resolve by key
     const uint32_t* bucket_of; // per node: bucket index or kNoId
+    const uint32_t* path_id;   // per node: pattern id naming keyed terminals below it, kNoId, or kKeep
     uint32_t groups;           // grouped format: uint4 records per node
     uint32_t depth_limit;      // 0 = untruncated
     const uint16_t* symtab;    // [256], kNoSym = byte outside the alphabet

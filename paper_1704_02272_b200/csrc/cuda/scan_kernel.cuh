@@ -266,7 +266,7 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 // is only used for depth <= min_emit, where nothing above can report.
 template <bool GROUPED, bool IDENT, bool PAR>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
-                                     uint32_t node, uint32_t depth, Sink& sink)
+                                     uint32_t node, uint32_t depth, Sink& sink, uint32_t pend = kNoId)
 {
     const TrieView& t = a.trie;
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
@@ -286,6 +286,9 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
         const uint32_t sym = IDENT ? byte : uint32_t(s_sym[byte]);
         const bool step = more && (IDENT || sym != kNoSym);
         uint32_t word, base, meta, inline_id = kNoId;
+        // the node's path id rides along with its record (same latency), so
+        // keyed terminals rarely need the slice lookup
+        const uint32_t pid = __ldg(t.path_id + node);
         if (GROUPED) {
             const uint32_t g = step ? (sym >> 6) : 0u;
             const uint4 r = __ldg(reinterpret_cast<const uint4*>(t.nodes) + (node * t.groups + g));
@@ -300,9 +303,10 @@ __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, u
             base = r.y & kBaseMask;
             meta = r.y;
         }
+        if (pid != kKeep) pend = pid;
         if (depth && (meta & kFlagTerminal)) {
             uint32_t id = GROUPED ? inline_id : __ldg(t.term_id + node);
-            if (id == kNoId) id = resolve_slice<PAR>(a, start, depth);
+            if (id == kNoId) id = pend != kNoId ? pend : resolve_slice<PAR>(a, start, depth);
             if (id == kNoId) atomicOr(a.err, 1u);
             else sink.put(a.g0 + start, depth, id);
         }
@@ -547,7 +551,7 @@ __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& 
 {
     if (h.aux.z & 1u) {
         uint32_t id = h.w.w;
-        if (id == kNoId) id = resolve_slice<PAR>(a, start, depth);
+        if (id == kNoId) id = h.aux.w != kNoId ? h.aux.w : resolve_slice<PAR>(a, start, depth);
         if (id == kNoId) atomicOr(a.err, 1u);
         else sink.put(a.g0 + start, depth, id);
     }
@@ -592,6 +596,7 @@ struct Walker {
             uint64_t win = 0;
             uint32_t node = 0, depth = 0;
             JumpHit hit{};
+            hit.aux.w = kNoId; // no jump: the walk starts at the root with no path id
             // k == limit: walks end at the jump node; the slot has what they emit
             const bool at_limit = KW != 0 && a.trie.jump_bits && a.trie.filter_k == a.trie.depth_limit;
             if (e < ns) {
@@ -610,7 +615,7 @@ struct Walker {
                 }
                 if (node != kNoId) {
                     if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
-                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink);
+                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink, hit.aux.w);
                 }
             }
             uint32_t tot;
@@ -627,7 +632,7 @@ struct Walker {
                     wr.cap = a.warp_cap;
                     wr.skip = kRegRecords;
                     if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
-                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr);
+                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr, hit.aux.w);
                 }
             }
             cursor += tot;

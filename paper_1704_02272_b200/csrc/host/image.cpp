@@ -28,7 +28,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -162,6 +162,45 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         if (node < n && node != 0 && t.terminal(node) && unique_path[node]) im.term_id[node] = uint32_t(id);
     }
 
+    // ---- path ids: keyed terminals named by the walk's path ------------------
+    // A pattern whose terminal is shared (keyed) is still determined by the
+    // deepest path-unique node U on its path when U leads to no other keyed
+    // terminal and no terminal lies between U and the end.  path_id[U] = that
+    // pattern (kNoId if U is ambiguous); path_id of a non-unique node = kKeep.
+    // The walk carries the last path_id it met and names a keyed terminal with
+    // it; only kNoId falls back to the slice-key lookup.
+    im.path_id.assign(n, kKeep);
+    {
+        for (uint32_t u = 0; u < n; ++u)
+            if (unique_path[u]) im.path_id[u] = kNoId;
+        std::vector<uint8_t> conflict(n, 0);
+        std::vector<uint32_t> path;
+        for (size_t id = 0; id < P; ++id) {
+            path.assign(1, 0u);
+            for (unsigned char c : t.patterns[id]) {
+                const uint32_t nx = t.transition(path.back(), c);
+                if (nx >= n) break;
+                path.push_back(nx);
+            }
+            const size_t L = path.size() - 1;
+            if (L != t.patterns[id].size()) continue; // truncated away
+            const uint32_t T = path[L];
+            if (!t.terminal(T) || im.term_id[T] != kNoId) continue; // private terminals name themselves
+            size_t u = L;
+            while (u > 0 && !unique_path[path[u]]) --u;
+            if (!unique_path[path[u]]) continue;
+            bool clean = true;
+            for (size_t i = u + 1; i < L; ++i) clean = clean && !t.terminal(path[i]);
+            const uint32_t U = path[u];
+            if (!clean || (im.path_id[U] != kNoId && im.path_id[U] != uint32_t(id))) conflict[U] = 1;
+            else im.path_id[U] = uint32_t(id);
+        }
+        for (uint32_t u = 0; u < n; ++u)
+            if (conflict[u]) im.path_id[u] = kNoId;
+    }
+    // the path id a walk carries after entering node v from a parent carrying `pend`
+    auto pend_at = [&](uint32_t v, uint32_t pend) { return im.path_id[v] != kKeep ? im.path_id[v] : pend; };
+
     // ---- buckets: CSR, each sorted by (length, id) -----------------------
     im.bucket_of.assign(n, kNoId);
     for (const auto& [node, ids] : t.buckets) {
@@ -271,13 +310,14 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         const uint32_t k = std::min(im.min_emit, kMaxFilterKey);
         im.filter_k = k;
         std::vector<uint64_t> grams;
-        std::vector<uint32_t> gram_node;
+        std::vector<uint32_t> gram_node, gram_pend;
         const uint64_t cap = uint64_t(1) << 22;
         struct Frame {
             uint32_t node, depth;
             uint64_t key;
+            uint32_t pend;
         };
-        std::vector<Frame> st{{0u, 0u, 0ull}};
+        std::vector<Frame> st{{0u, 0u, 0ull, pend_at(0, kNoId)}};
         bool overflow = false;
         while (!st.empty() && !overflow) {
             Frame f = st.back();
@@ -285,6 +325,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             if (f.depth == k) {
                 grams.push_back(f.key);
                 gram_node.push_back(f.node);
+                gram_pend.push_back(f.pend);
                 overflow = grams.size() > cap;
                 continue;
             }
@@ -294,7 +335,8 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 for (uint32_t bits = c[w]; bits; bits &= bits - 1) {
                     const uint32_t s = w * 32 + uint32_t(__builtin_ctz(bits));
                     const uint64_t b = t.alphabet.byte_of(s);
-                    st.push_back({child++, f.depth + 1, f.key | (b << (8 * f.depth))});
+                    st.push_back({child, f.depth + 1, f.key | (b << (8 * f.depth)), pend_at(child, f.pend)});
+                    ++child;
                 }
         }
         im.filter_paths = grams.size();
@@ -436,6 +478,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
                     slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
                     slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
+                    slot[7] = gram_pend[i];
                 }
             }
         }
@@ -454,11 +497,11 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         const uint32_t sb = sigma <= 2 ? 1u : (sigma <= 4 ? 2u : 0u);
         const uint32_t ks = sb && im.min_emit != UINT32_MAX ? std::min(im.min_emit, 32u / sb) : 0u;
         if (opt.symbol_keys && sb && ks > std::min(im.min_emit, kMaxFilterKey) && opt.jump) {
-            std::vector<uint32_t> keys, knode;
+            std::vector<uint32_t> keys, knode, kpend;
             struct SFrame {
-                uint32_t node, depth, key;
+                uint32_t node, depth, key, pend;
             };
-            std::vector<SFrame> st{{0u, 0u, 0u}};
+            std::vector<SFrame> st{{0u, 0u, 0u, pend_at(0, kNoId)}};
             bool overflow = false;
             while (!st.empty() && !overflow) {
                 const SFrame f = st.back();
@@ -466,6 +509,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 if (f.depth == ks) {
                     keys.push_back(f.key);
                     knode.push_back(f.node);
+                    kpend.push_back(f.pend);
                     overflow = keys.size() > (uint64_t(1) << 22);
                     continue;
                 }
@@ -474,7 +518,8 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 for (uint32_t w = 0; w < t.words; ++w)
                     for (uint32_t bits = c[w]; bits; bits &= bits - 1) {
                         const uint32_t s = w * 32 + uint32_t(__builtin_ctz(bits));
-                        st.push_back({child++, f.depth + 1, f.key | (s << (sb * f.depth))});
+                        st.push_back({child, f.depth + 1, f.key | (s << (sb * f.depth)), pend_at(child, f.pend)});
+                        ++child;
                     }
             }
             if (!overflow && !keys.empty()) {
@@ -514,6 +559,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
                     slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
                     slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
+                    slot[7] = kpend[i];
                 }
             }
         }

@@ -15,6 +15,7 @@ struct GpuImage {
     uint32_t groups = 0; // 0 = narrow uint2 records, else uint4 records per node
     std::vector<uint32_t> nodes;
     std::vector<uint32_t> term_id, bucket_of;
+    std::vector<uint32_t> path_id; // per node: see image.cpp "path ids" (kKeep on non-unique nodes)
     bool identity = false;
     std::array<uint16_t, 256> symtab{};
     uint32_t depth_limit = 0;
