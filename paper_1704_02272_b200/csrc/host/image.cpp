@@ -169,8 +169,53 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     // pattern (kNoId if U is ambiguous); path_id of a non-unique node = kKeep.
     // The walk carries the last path_id it met and names a keyed terminal with
     // it; only kNoId falls back to the slice-key lookup.
-    im.path_id.assign(n, kKeep);
+    // They are only sound when the trie accepts exactly its dictionary (true
+    // for every trie this library builds or compresses; a hand-made .htri may
+    // carry terminals that spell no pattern, which must keep failing like the
+    // reference).  Check: the number of root-to-terminal paths (Kahn order over
+    // the DAG; a cycle disables path ids) equals the number of patterns whose
+    // full path ends at a terminal.
+    bool dictionary_language = true;
     {
+        std::vector<uint32_t> deg = indeg, order;
+        order.reserve(n);
+        if (deg[0] != 0) dictionary_language = false;
+        else order.push_back(0);
+        for (size_t h = 0; h < order.size(); ++h) {
+            const uint32_t u = order[h];
+            for (uint32_t i = 0; i < kids[u]; ++i)
+                if (--deg[t.offset(u) + i] == 0) order.push_back(t.offset(u) + i);
+        }
+        std::vector<uint64_t> paths(n, 0);
+        uint64_t terminal_paths = 0;
+        constexpr uint64_t kCap = uint64_t(1) << 62;
+        if (dictionary_language) {
+            paths[0] = 1;
+            for (uint32_t u : order) {
+                if (u != 0 && t.terminal(u)) terminal_paths = std::min(kCap, terminal_paths + paths[u]);
+                for (uint32_t i = 0; i < kids[u]; ++i) {
+                    uint64_t& c = paths[t.offset(u) + i];
+                    c = std::min(kCap, c + paths[u]);
+                }
+            }
+        }
+        uint64_t spelled = 0;
+        for (size_t id = 0; id < P && dictionary_language; ++id) {
+            uint32_t node = 0;
+            bool full = true;
+            for (unsigned char c : t.patterns[id]) {
+                node = t.transition(node, c);
+                if (node >= n) {
+                    full = false;
+                    break;
+                }
+            }
+            spelled += (full && node != 0 && t.terminal(node)) ? 1u : 0u;
+        }
+        dictionary_language = dictionary_language && order.size() == n && terminal_paths == spelled;
+    }
+    im.path_id.assign(n, kKeep);
+    if (dictionary_language) {
         for (uint32_t u = 0; u < n; ++u)
             if (unique_path[u]) im.path_id[u] = kNoId;
         std::vector<uint8_t> conflict(n, 0);
