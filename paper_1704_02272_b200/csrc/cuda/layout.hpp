@@ -93,8 +93,10 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 
 // Jump table: every depth-k path string (k = filter_k bytes, little-endian in
 // {lo, hi}) -> the node it reaches.  No node above depth k can report
-// (k <= min_emit), so a walk may start there instead of at the root.  Open
-// addressing, load <= 1/2, 32-byte slots
+// (k <= min_emit), so a walk may start there instead of at the root.  Cuckoo
+// hashing: a key lives in slot jump_slot or jump_slot2, so a lookup is two
+// independent loads and no probe loop (a linear-probing loop ran up to the
+// slowest lane's chain length per warp).  32-byte slots
 //   {lo, hi, node, term, bk_first, bk_count, flags, pend}
 // node == kNoId marks an empty slot.  The rest describes the node itself, so a
 // walk that starts at the depth limit (truncated tries with k == limit) emits
@@ -103,6 +105,10 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 // pend = the path id a walk carries at the node (image.cpp "path ids").
 constexpr uint32_t kJumpWords = 8;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
+HFB_HD uint32_t jump_slot2(uint32_t key32, uint32_t bits)
+{
+    return filter2_hash(key32 * 0x9E3779B1u + 0x7F4A7C15u) >> (32 - bits);
+}
 
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {

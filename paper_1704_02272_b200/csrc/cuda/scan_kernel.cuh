@@ -490,16 +490,21 @@ struct JumpHit {
     uint4 w;   // {lo, hi, node, term}
     uint4 aux; // {bk_first, bk_count, flags, 0}
 };
+// Cuckoo lookup (layout.hpp): both candidate slots load at once.
 __device__ __forceinline__ JumpHit jump_lookup_key(const TrieView& t, uint32_t lo, uint32_t hi)
 {
-    const uint32_t mask = (1u << t.jump_bits) - 1u;
     const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
-    for (uint32_t s = jump_slot(lo ^ (hi * 0x85EBCA77u), t.jump_bits);; s = (s + 1) & mask) {
-        JumpHit h;
-        h.w = __ldg(slots + 2 * s);
-        h.aux = __ldg(slots + 2 * s + 1);
-        if (h.w.z == kNoId || (h.w.x == lo && h.w.y == hi)) return h;
-    }
+    const uint32_t k32 = lo ^ (hi * 0x85EBCA77u);
+    const uint32_t s1 = jump_slot(k32, t.jump_bits), s2 = jump_slot2(k32, t.jump_bits);
+    JumpHit a, b;
+    a.w = __ldg(slots + 2 * s1);
+    a.aux = __ldg(slots + 2 * s1 + 1);
+    b.w = __ldg(slots + 2 * s2);
+    b.aux = __ldg(slots + 2 * s2 + 1);
+    if (a.w.z != kNoId && a.w.x == lo && a.w.y == hi) return a;
+    if (b.w.z != kNoId && b.w.x == lo && b.w.y == hi) return b;
+    a.w.z = kNoId;
+    return a;
 }
 
 // Symbol-key mode: the first filter_k symbols of the start, packed sym_bits
@@ -532,14 +537,7 @@ __device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
     uint32_t lo = uint32_t(win), hi = 0;
     if (KW == 1) lo &= (1u << (8 * k)) - 1u;
     if (KW == 2) hi = uint32_t(win >> 32) & (k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u));
-    const uint32_t mask = (1u << t.jump_bits) - 1u;
-    const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
-    for (uint32_t s = jump_slot(lo ^ (hi * 0x85EBCA77u), t.jump_bits);; s = (s + 1) & mask) {
-        JumpHit h;
-        h.w = __ldg(slots + 2 * s);
-        h.aux = __ldg(slots + 2 * s + 1); // same 32-byte sector: no extra latency
-        if (h.w.z == kNoId || (h.w.x == lo && h.w.y == hi)) return h;
-    }
+    return jump_lookup_key(t, lo, hi);
 }
 
 // A walk that starts at the depth limit (k == limit): the node's terminal

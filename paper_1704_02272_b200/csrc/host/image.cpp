@@ -17,6 +17,7 @@
 #include "image.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -63,6 +64,56 @@ uint32_t ceil_log2(uint64_t x)
     uint32_t b = 0;
     while ((uint64_t(1) << b) < x) ++b;
     return b;
+}
+
+// Cuckoo jump table (layout.hpp): entries are 8-word slots whose words 0/1
+// are the key; a slot with word 2 == kNoId is empty.  Grows until every key
+// places (load <= 1/2 to start).
+void build_jump_table(GpuImage& im, const std::vector<std::array<uint32_t, kJumpWords>>& entries)
+{
+    constexpr size_t W = kJumpWords;
+    uint32_t jb = std::max<uint32_t>(ceil_log2(entries.size()) + 1, 4);
+    for (;; ++jb) {
+        const size_t slots = size_t(1) << jb;
+        std::vector<uint32_t> tab(W * slots, 0u);
+        for (size_t s = 0; s < slots; ++s) tab[W * s + 2] = kNoId;
+        bool ok = true;
+        for (size_t i = 0; i < entries.size() && ok; ++i) {
+            std::array<uint32_t, kJumpWords> cur = entries[i];
+            uint32_t pos = jump_slot(cur[0] ^ (cur[1] * 0x85EBCA77u), jb);
+            for (int kick = 0;; ++kick) {
+                if (kick > 500) {
+                    ok = false;
+                    break;
+                }
+                uint32_t* slot = &tab[W * pos];
+                if (slot[2] == kNoId) {
+                    std::copy(cur.begin(), cur.end(), slot);
+                    break;
+                }
+                const uint32_t k32 = cur[0] ^ (cur[1] * 0x85EBCA77u);
+                const uint32_t alt = pos == jump_slot(k32, jb) ? jump_slot2(k32, jb) : jump_slot(k32, jb);
+                uint32_t* other = &tab[W * alt];
+                if (other[2] == kNoId) {
+                    std::copy(cur.begin(), cur.end(), other);
+                    break;
+                }
+                // evict the occupant of `pos` and move it to its other slot
+                std::array<uint32_t, kJumpWords> ev;
+                std::copy(slot, slot + W, ev.begin());
+                std::copy(cur.begin(), cur.end(), slot);
+                cur = ev;
+                const uint32_t ek = cur[0] ^ (cur[1] * 0x85EBCA77u);
+                pos = pos == jump_slot(ek, jb) ? jump_slot2(ek, jb) : jump_slot(ek, jb);
+            }
+        }
+        if (ok) {
+            im.jump_bits = jb;
+            im.jump = std::move(tab);
+            return;
+        }
+        if (jb > 30) fail(HEPFAC_ERR_NOMEM, "cannot place the jump table");
+    }
 }
 
 } // namespace
@@ -504,30 +555,20 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 }
             }
             if (opt.jump) {
-                const uint32_t jb = std::max<uint32_t>(ceil_log2(grams.size()) + 1, 4);
-                const uint32_t mask = (1u << jb) - 1u;
-                im.jump_bits = jb;
-                constexpr size_t W = kJumpWords;
-                im.jump.assign(W << jb, 0u);
-                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[W * s + 2] = kNoId;
+                std::vector<std::array<uint32_t, kJumpWords>> entries(grams.size());
                 for (size_t i = 0; i < grams.size(); ++i) {
-                    uint32_t s = jump_slot(filter_fold(grams[i]), jb);
-                    while (im.jump[W * s + 2] != kNoId) s = (s + 1) & mask;
                     const uint32_t node = gram_node[i];
-                    uint32_t* slot = &im.jump[W * s];
-                    slot[0] = uint32_t(grams[i]);
-                    slot[1] = uint32_t(grams[i] >> 32);
-                    slot[2] = node;
-                    slot[3] = im.term_id[node];
                     const uint32_t b = im.bucket_of[node];
-                    slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
-                    slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
-                    slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
-                    slot[7] = gram_pend[i];
+                    entries[i] = {uint32_t(grams[i]), uint32_t(grams[i] >> 32), node, im.term_id[node],
+                                  b == kNoId ? 0u : im.bk_span[2 * size_t(b)],
+                                  b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
+                                  (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), gram_pend[i]};
                 }
+                build_jump_table(im, entries);
             }
         }
     }
+
     // ---- symbol-key mode (small alphabets) -----------------------------------
     // Byte keys carry log2(sigma) bits per byte: 8 bytes of DNA are 16 bits, of
     // a binary alphabet 8.  When the shortest report depth allows more than 8
@@ -585,27 +626,16 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 im.filter2.clear();
                 im.key4.clear();
                 im.lean_single = false;
-                const uint32_t jb = std::max<uint32_t>(ceil_log2(keys.size()) + 1, 4);
-                const uint32_t mask = (1u << jb) - 1u;
-                constexpr size_t W = kJumpWords;
-                im.jump_bits = jb;
-                im.jump.assign(W << jb, 0u);
-                for (size_t s = 0; s < (size_t(1) << jb); ++s) im.jump[W * s + 2] = kNoId;
+                std::vector<std::array<uint32_t, kJumpWords>> entries(keys.size());
                 for (size_t i = 0; i < keys.size(); ++i) {
-                    uint32_t s = jump_slot(keys[i], jb); // filter_fold(key) == key for 32-bit keys
-                    while (im.jump[W * s + 2] != kNoId) s = (s + 1) & mask;
                     const uint32_t node = knode[i];
-                    uint32_t* slot = &im.jump[W * s];
-                    slot[0] = keys[i];
-                    slot[1] = 0;
-                    slot[2] = node;
-                    slot[3] = im.term_id[node];
                     const uint32_t b = im.bucket_of[node];
-                    slot[4] = b == kNoId ? 0u : im.bk_span[2 * size_t(b)];
-                    slot[5] = b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1];
-                    slot[6] = (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u);
-                    slot[7] = kpend[i];
+                    entries[i] = {keys[i], 0u, node, im.term_id[node],
+                                  b == kNoId ? 0u : im.bk_span[2 * size_t(b)],
+                                  b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
+                                  (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), kpend[i]};
                 }
+                build_jump_table(im, entries);
             }
         }
     }
