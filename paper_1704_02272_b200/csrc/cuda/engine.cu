@@ -253,6 +253,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.filter2_bits = im.filter2_bits;
     v.jump = d->upload(im.jump);
     v.jump_bits = im.jump_bits;
+    v.jump_ext = im.jump_ext.empty() ? nullptr : d->upload(im.jump_ext);
     v.min_emit = im.min_emit;
 
     d->lean_single = im.filter_mode == 1 && im.lean_single;

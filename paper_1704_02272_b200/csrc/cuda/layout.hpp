@@ -104,6 +104,12 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 // pattern id (kNoId = resolve by key), flags bit 0 terminal, bit 1 bucket,
 // pend = the path id a walk carries at the node (image.cpp "path ids").
 constexpr uint32_t kJumpWords = 8;
+// Extension slots (k == limit, tables up to 2^kMaxJumpExtBits slots), parallel
+// to the jump table: {id, len, off_lo, off_hi} of the bucket's first entry and
+// its pattern bytes [limit & ~3, +16), zero padded.  A walk at the limit then
+// verifies that entry against the text without a bucket or pattern load.
+constexpr uint32_t kJumpExtWords = 8;
+constexpr uint32_t kMaxJumpExtBits = 20;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 HFB_HD uint32_t jump_slot2(uint32_t key32, uint32_t bits)
 {
@@ -141,6 +147,7 @@ struct TrieView {
     uint32_t key4_words;     // (single-probe hash, layout above); 0 = none
     const uint32_t* jump;    // 2^jump_bits uint4 slots
     uint32_t jump_bits;      // 0 = no jump table (walks start at the root)
+    const uint32_t* jump_ext; // per slot: first bucket entry + its next 16 pattern bytes, or null
     uint32_t min_emit;
 };
 

@@ -488,9 +488,12 @@ __device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
 // (`win` = text[start, start + 8)); w.z == kNoId when no trie path spells them.
 struct JumpHit {
     uint4 w;   // {lo, hi, node, term}
-    uint4 aux; // {bk_first, bk_count, flags, 0}
+    uint4 aux; // {bk_first, bk_count, flags, pend}
+    uint32_t slot;
 };
-// Cuckoo lookup (layout.hpp): both candidate slots load at once.
+// Cuckoo lookup (layout.hpp): both candidate slots load at once.  (Loading
+// both slots' extensions here as well cost the fused kernel 40% on c2:
+// register spills; emit_at_limit loads the chosen one.)
 __device__ __forceinline__ JumpHit jump_lookup_key(const TrieView& t, uint32_t lo, uint32_t hi)
 {
     const uint4* slots = reinterpret_cast<const uint4*>(t.jump);
@@ -499,8 +502,10 @@ __device__ __forceinline__ JumpHit jump_lookup_key(const TrieView& t, uint32_t l
     JumpHit a, b;
     a.w = __ldg(slots + 2 * s1);
     a.aux = __ldg(slots + 2 * s1 + 1);
+    a.slot = s1;
     b.w = __ldg(slots + 2 * s2);
     b.aux = __ldg(slots + 2 * s2 + 1);
+    b.slot = s2;
     if (a.w.z != kNoId && a.w.x == lo && a.w.y == hi) return a;
     if (b.w.z != kNoId && b.w.x == lo && b.w.y == hi) return b;
     a.w.z = kNoId;
@@ -547,13 +552,59 @@ template <bool PAR>
 __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& h, uint64_t start, uint32_t depth,
                                               Sink& sink)
 {
+    const TrieView& t = a.trie;
     if (h.aux.z & 1u) {
         uint32_t id = h.w.w;
         if (id == kNoId) id = h.aux.w != kNoId ? h.aux.w : resolve_slice<PAR>(a, start, depth);
         if (id == kNoId) atomicOr(a.err, 1u);
         else sink.put(a.g0 + start, depth, id);
     }
-    if (h.aux.z & 2u) verify_span(a, make_uint2(h.aux.x, h.aux.y), start, sink);
+    if (!(h.aux.z & 2u)) return;
+    uint2 span = make_uint2(h.aux.x, h.aux.y);
+    if (t.jump_ext) {
+        // The slot's extension has the first entry and its next 16 bytes:
+        // compare them against the text (an L1 hit next to the window just
+        // read), and touch the pattern only past those 16 bytes.
+        const uint32_t skip = t.depth_limit & ~3u;
+        const uint4* ext = reinterpret_cast<const uint4*>(t.jump_ext) + 2 * h.slot;
+        const uint4 en = __ldg(ext), pv = __ldg(ext + 1);
+        if (start + en.y <= a.n_avail) {
+            const uint64_t p = start + skip;
+            const uint32_t* tw = reinterpret_cast<const uint32_t*>(a.text + (p & ~3ull));
+            const uint32_t sh = uint32_t(p & 3u) * 8u;
+            uint32_t tx[5];
+#pragma unroll
+            for (uint32_t k = 0; k < 5; ++k) tx[k] = __ldg(tw + k); // padded text: safe to overread
+            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+            const uint32_t rem = en.y - skip;
+            uint32_t diff = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if (4 * k < rem) diff |= ((sh ? __funnelshift_r(tx[k], tx[k + 1], sh) : tx[k]) ^ pw[k]) & tail_mask(rem - 4 * k);
+            if (!diff && (rem <= 16 || same_at(a, p + 16, ((uint64_t(en.w) << 32) | en.z) + skip + 16, rem - 16)))
+                sink.put(a.g0 + start, en.y, en.x);
+        }
+        ++span.x;
+        --span.y;
+    }
+    verify_span(a, span, start, sink);
+}
+
+// A start with more records than the registers hold (rare): walk it again and
+// write records kRegRecords.. directly.  Out of line, so each flush carries
+// one copy of the walk.
+template <bool GROUPED, bool IDENT, bool PAR>
+__device__ __noinline__ void rewalk_rest(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
+                                         uint32_t node, uint32_t depth, JumpHit hit, bool at_limit,
+                                         hepfac_match_t* region, uint64_t at)
+{
+    Sink wr;
+    wr.dst = region;
+    wr.at = at;
+    wr.cap = a.warp_cap;
+    wr.skip = kRegRecords;
+    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
+    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr, hit.aux.w);
 }
 
 template <bool GROUPED, bool IDENT, int KW, bool PAR>
@@ -623,15 +674,9 @@ struct Walker {
                 uint4* dst = reinterpret_cast<uint4*>(region);
                 if (at < a.warp_cap) dst[at] = sink.r0;
                 if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
-                if (sink.n > kRegRecords) { // rare: re-walk and write the rest directly
-                    Sink wr;
-                    wr.dst = region;
-                    wr.at = at + kRegRecords;
-                    wr.cap = a.warp_cap;
-                    wr.skip = kRegRecords;
-                    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
-                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr, hit.aux.w);
-                }
+                if (sink.n > kRegRecords) // rare: re-walk and write the rest directly
+                    rewalk_rest<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, hit, at_limit, region,
+                                                     at + kRegRecords);
             }
             cursor += tot;
         }
@@ -845,7 +890,13 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
         const uint32_t rem = start_end > lo ? uint32_t(min(start_end - lo, uint64_t(kTile))) : 0u;
         const uint32_t fetched = uint32_t(min((stop - lo + kGroup - 1) / kGroup, uint64_t(kGroupsPerTile)));
         uint32_t qn = 0;
-        for (uint32_t g = 0; g < fetched; ++g) {
+        // g == fetched is the tile's last flush: one call site keeps one
+        // inlined copy of the walk in the kernel
+        for (uint32_t g = 0;; ++g) {
+            if (g == fetched) {
+                if (qn) wk.flush(lo, qn);
+                break;
+            }
             // slice s of this lane: group starts [s * 512 + 16 * lane, +16)
             uint32_t valid[kSlices];
 #pragma unroll
@@ -917,7 +968,6 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                 __syncwarp();
             }
         }
-        if (qn) wk.flush(lo, qn);
         if (lane == 0) {
             a.tile_count[tile] = uint32_t(wk.cursor - slot);
             a.tile_slot[tile] = uint32_t(slot);

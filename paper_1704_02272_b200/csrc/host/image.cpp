@@ -29,7 +29,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + jump_ext.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -44,6 +44,7 @@ ImageOptions image_options_from_env()
         if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
     }
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
+    if (const char* s = std::getenv("HEPFAC_JUMP_EXT")) o.jump_ext = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_LEAN_SINGLE")) o.lean_single = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
@@ -68,18 +69,25 @@ uint32_t ceil_log2(uint64_t x)
 
 // Cuckoo jump table (layout.hpp): entries are 8-word slots whose words 0/1
 // are the key; a slot with word 2 == kNoId is empty.  Grows until every key
-// places (load <= 1/2 to start).
-void build_jump_table(GpuImage& im, const std::vector<std::array<uint32_t, kJumpWords>>& entries)
+// places (load <= 1/2 to start).  When the walks start at the depth limit
+// (k == limit) and the table stays L2-sized, each slot also gets its
+// extension (layout.hpp kJumpExtWords): the bucket's first entry and that
+// pattern's 16 bytes after the last 4-byte boundary below the limit.
+using JumpEntry = std::array<uint32_t, kJumpWords>;
+
+void build_jump_table(GpuImage& im, const std::vector<JumpEntry>& entries, bool ext)
 {
     constexpr size_t W = kJumpWords;
     uint32_t jb = std::max<uint32_t>(ceil_log2(entries.size()) + 1, 4);
     for (;; ++jb) {
         const size_t slots = size_t(1) << jb;
         std::vector<uint32_t> tab(W * slots, 0u);
+        std::vector<uint32_t> where(slots, kNoId); // slot -> entry index
         for (size_t s = 0; s < slots; ++s) tab[W * s + 2] = kNoId;
         bool ok = true;
         for (size_t i = 0; i < entries.size() && ok; ++i) {
-            std::array<uint32_t, kJumpWords> cur = entries[i];
+            JumpEntry cur = entries[i];
+            uint32_t ci = uint32_t(i);
             uint32_t pos = jump_slot(cur[0] ^ (cur[1] * 0x85EBCA77u), jb);
             for (int kick = 0;; ++kick) {
                 if (kick > 500) {
@@ -89,6 +97,7 @@ void build_jump_table(GpuImage& im, const std::vector<std::array<uint32_t, kJump
                 uint32_t* slot = &tab[W * pos];
                 if (slot[2] == kNoId) {
                     std::copy(cur.begin(), cur.end(), slot);
+                    where[pos] = ci;
                     break;
                 }
                 const uint32_t k32 = cur[0] ^ (cur[1] * 0x85EBCA77u);
@@ -96,13 +105,17 @@ void build_jump_table(GpuImage& im, const std::vector<std::array<uint32_t, kJump
                 uint32_t* other = &tab[W * alt];
                 if (other[2] == kNoId) {
                     std::copy(cur.begin(), cur.end(), other);
+                    where[alt] = ci;
                     break;
                 }
                 // evict the occupant of `pos` and move it to its other slot
-                std::array<uint32_t, kJumpWords> ev;
+                JumpEntry ev;
                 std::copy(slot, slot + W, ev.begin());
+                const uint32_t ei = where[pos];
                 std::copy(cur.begin(), cur.end(), slot);
+                where[pos] = ci;
                 cur = ev;
+                ci = ei;
                 const uint32_t ek = cur[0] ^ (cur[1] * 0x85EBCA77u);
                 pos = pos == jump_slot(ek, jb) ? jump_slot2(ek, jb) : jump_slot(ek, jb);
             }
@@ -110,6 +123,21 @@ void build_jump_table(GpuImage& im, const std::vector<std::array<uint32_t, kJump
         if (ok) {
             im.jump_bits = jb;
             im.jump = std::move(tab);
+            im.jump_ext.clear();
+            if (ext && jb <= kMaxJumpExtBits) {
+                const uint32_t skip = im.depth_limit & ~3u;
+                im.jump_ext.assign(kJumpExtWords * slots, 0u);
+                for (size_t s = 0; s < slots; ++s) {
+                    const uint32_t* slot = &im.jump[W * s];
+                    if (where[s] == kNoId || !(slot[6] & 2u)) continue;
+                    uint32_t* x = &im.jump_ext[kJumpExtWords * s];
+                    std::copy_n(&im.bk_entry[4 * size_t(slot[4])], 4, x);
+                    const uint32_t len = x[1];
+                    const uint64_t off = (uint64_t(x[3]) << 32) | x[2];
+                    for (uint32_t b = skip; b < std::min(len, skip + 16); ++b)
+                        x[4 + (b - skip) / 4] |= uint32_t(im.pat_bytes[off + b]) << (8 * ((b - skip) & 3));
+                }
+            }
             return;
         }
         if (jb > 30) fail(HEPFAC_ERR_NOMEM, "cannot place the jump table");
@@ -555,7 +583,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 }
             }
             if (opt.jump) {
-                std::vector<std::array<uint32_t, kJumpWords>> entries(grams.size());
+                std::vector<JumpEntry> entries(grams.size());
                 for (size_t i = 0; i < grams.size(); ++i) {
                     const uint32_t node = gram_node[i];
                     const uint32_t b = im.bucket_of[node];
@@ -564,7 +592,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                                   b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
                                   (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), gram_pend[i]};
                 }
-                build_jump_table(im, entries);
+                build_jump_table(im, entries, opt.jump_ext && im.depth_limit != 0 && im.filter_k == im.depth_limit);
             }
         }
     }
@@ -626,7 +654,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 im.filter2.clear();
                 im.key4.clear();
                 im.lean_single = false;
-                std::vector<std::array<uint32_t, kJumpWords>> entries(keys.size());
+                std::vector<JumpEntry> entries(keys.size());
                 for (size_t i = 0; i < keys.size(); ++i) {
                     const uint32_t node = knode[i];
                     const uint32_t b = im.bucket_of[node];
@@ -635,13 +663,13 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                                   b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
                                   (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), kpend[i]};
                 }
-                build_jump_table(im, entries);
+                build_jump_table(im, entries, opt.jump_ext && im.depth_limit != 0 && im.filter_k == im.depth_limit);
             }
         }
     }
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
-    if (im.jump.empty()) im.jump.assign(kJumpWords, 0u);
+    if (im.jump.empty()) im.jump.assign(kJumpWords, 0u), im.jump_ext.clear();
 
     for (uint32_t u = 0; u < n; ++u)
         if (t.terminal(u) && u != 0) (im.term_id[u] == kNoId ? im.keyed_terminals : im.private_terminals)++;

@@ -354,6 +354,46 @@ def test_lean_single_pipeline(gpu, monkeypatch, stages, depth):
     assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
 
 
+@pytest.mark.parametrize("ext", ["1", "0"])
+@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("sigma,depth", [(4, 8), (20, 5), (256, 4)])
+def test_depth_limit_buckets(gpu, monkeypatch, sigma, depth, two_pass, ext):
+    # Walks that start at the depth limit (filter_k == limit) emit from the
+    # jump slot; with HEPFAC_JUMP_EXT the bucket's first entry and its next 16
+    # bytes come from the slot's extension.  Buckets of 1..6 entries, lengths
+    # from the limit to 40 past it (compares beyond the inline 16 bytes),
+    # near misses in the last byte, and copies overhanging the text end.
+    monkeypatch.setenv("HEPFAC_JUMP_EXT", ext)
+    if two_pass:
+        monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
+    rng = np.random.default_rng(500 + sigma + depth)
+    a, syms = alphabet_bytes(gpu, sigma)
+    pats = set()
+    for _ in range(60):
+        head = bytes(syms[rng.integers(0, syms.size, size=depth)])
+        if rng.random() < 0.3:
+            pats.add(head)
+        body = bytes(syms[rng.integers(0, syms.size, size=40)])
+        for _ in range(int(rng.integers(1, 7))):
+            n = int(rng.integers(1, 41))
+            tail = bytearray(body[:n])
+            tail[-1] = int(syms[rng.integers(0, syms.size)])
+            pats.add(head + bytes(tail))
+    pats = sorted(pats)
+    t = build(gpu, pats, sigma, 1, depth)
+    assert gpu.layout_info(t)["filter_k"] == depth
+    tx = text(rng, syms, 200000)
+    for i, p in enumerate(pats):
+        at = int(rng.integers(0, tx.size - 64))
+        plant(tx, p, at)
+        miss = bytearray(p)
+        miss[-1] = int(syms[(np.searchsorted(syms, miss[-1]) + 1) % syms.size])
+        plant(tx, bytes(miss), int(rng.integers(0, tx.size - 64)))
+    longest = max(pats, key=len)
+    tx[-(len(longest) - 1):] = np.frombuffer(longest[:-1], dtype=np.uint8)
+    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
+
+
 @pytest.mark.parametrize("sigma", [2, 4])
 def test_symbol_key_mode(gpu, sigma):
     # small alphabets with long shortest patterns: filter and jump keys are
