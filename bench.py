@@ -199,6 +199,10 @@ def cpu_reference_gbps(w, trie_state: str, sample: np.ndarray, runs: int = 3):
     if ref is not None:
         t, _ = workloads.build_trie(ref, w, trie_state)
         rep = ref.run_throughput(t, sample, runs=runs, workers=cores)
+        # also one worker, on a smaller slice of the same sample
+        one = sample[: min(sample.size, 32 << 20)]
+        rep["single_worker"] = {"value": round(ref.run_throughput(t, one, runs=runs, workers=1)["gbps"], 4),
+                                "sample_bytes": int(one.size)}
         return rep["gbps"], cores, "reference", rep
     # port: the C restatement, one core
     from paper_1704_02272_b200 import hepfac
@@ -373,6 +377,11 @@ def main():
         out["cpu_baseline"] = {"value": round(g, 4), "unit": UNIT, "cores": cores, "kind": kind,
                                "sample": f"first {sample.size >> 20} MiB of the same text; "
                                          f"hepfac_run_throughput walk-phase mean of 3 runs after 1 warm-up"}
+        if "single_worker" in rep:
+            sw = rep["single_worker"]
+            out["cpu_baseline"]["single_worker"] = {
+                "value": sw["value"], "unit": UNIT, "cores": 1,
+                "sample": f"first {sw['sample_bytes'] >> 20} MiB of the same text, same timing"}
     if d.rank == 0:
         print(json.dumps(out))
     d.close()
