@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--states", default="s1trunc,stage2")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--check", action="store_true", help="compare with the compiled reference on 16 MiB")
+    ap.add_argument("--full-check", action="store_true",
+                    help="compare the whole text's match array with the compiled reference (memcmp + SHA-256)")
     args = ap.parse_args()
     lib = hepfac.lib()
     for spec in args.configs.split(","):
@@ -63,6 +65,22 @@ def main():
                 want = ref.scan(rt, sub, workers=os.cpu_count())
                 got = lib.scan(trie, sub)
                 rec["parity_16MiB"] = bool(got.shape == want.shape and (got == want).all())
+            if args.full_check:
+                import hashlib
+
+                import oracle
+                ref = oracle.ref_library()
+                rt, _ = workloads.build_trie(ref, w, state)
+                t2 = time.perf_counter()
+                want = ref.scan(rt, text, workers=os.cpu_count())
+                ref_s = time.perf_counter() - t2
+                got = lib.scan(trie, text)
+                rec["parity_full"] = {
+                    "equal": bool(got.shape == want.shape and got.tobytes() == want.tobytes()),
+                    "matches": int(got.size), "ref_matches": int(want.size),
+                    "sha256": hashlib.sha256(got.tobytes()).hexdigest(),
+                    "ref_sha256": hashlib.sha256(want.tobytes()).hexdigest(),
+                    "ref_scan_s": round(ref_s, 2), "ref_workers": os.cpu_count()}
             print(json.dumps(rec), flush=True)
 
 
