@@ -561,6 +561,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
             dt.pack_fn<<<std::max(1u, blocks), 256, 0, ws.stream>>>(d_text, words, dt.view.symtab, ws.d_packed);
             CK(cudaGetLastError());
             f.packed = ws.d_packed;
+            a.packed = ws.d_packed;
         }
         dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());

@@ -104,12 +104,21 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 // pattern id (kNoId = resolve by key), flags bit 0 terminal, bit 1 bucket,
 // pend = the path id a walk carries at the node (image.cpp "path ids").
 constexpr uint32_t kJumpWords = 8;
-// Extension slots (k == limit, tables up to 2^kMaxJumpExtBits slots), parallel
-// to the jump table: {id, len, off_lo, off_hi} of the bucket's first entry and
-// its pattern bytes [limit & ~3, +16), zero padded.  A walk at the limit then
-// verifies that entry against the text without a bucket or pattern load.
-constexpr uint32_t kJumpExtWords = 8;
-constexpr uint32_t kMaxJumpExtBits = 20;
+// Inline pattern lists: when at most kJumpExtEntries patterns start with a
+// slot's key (flags bit 2 = kJumpInline, the count in bits 3-4), the parallel
+// extension table (tables up to 2^kMaxJumpExtBits slots) holds each as {id,
+// len, 24 pattern bytes [inline_skip, +24), zero padded}, in (length, id) order.
+// They are every record a start with that key can emit (the trie accepts
+// exactly its dictionary), so instead of walking the subtree (or reading the
+// terminal and bucket at the depth limit) the start verifies them against the
+// text with one extension load.
+constexpr uint32_t kJumpInline = 4u;
+constexpr uint32_t kJumpInlineShift = 3u;
+constexpr uint32_t kJumpExtEntries = 2;
+constexpr uint32_t kJumpExtEntryWords = 8;
+constexpr uint32_t kJumpExtBytes = 4 * (kJumpExtEntryWords - 2);
+constexpr uint32_t kJumpExtWords = kJumpExtEntries * kJumpExtEntryWords;
+constexpr uint32_t kMaxJumpExtBits = 19;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 HFB_HD uint32_t jump_slot2(uint32_t key32, uint32_t bits)
 {
@@ -150,5 +159,10 @@ struct TrieView {
     const uint32_t* jump_ext; // per slot: first bucket entry + its next 16 pattern bytes, or null
     uint32_t min_emit;
 };
+
+// First pattern byte an inline list entry stores (kJumpExtBytes from there):
+// byte keys matched bytes [0, k) exactly; packed symbol keys did not (bytes
+// outside the alphabet pack as symbol 0), so their compare starts at byte 0.
+HFB_HD uint32_t inline_skip(uint32_t filter_k, uint32_t sym_bits) { return sym_bits ? 0u : filter_k & ~3u; }
 
 } // namespace hfb

@@ -103,6 +103,7 @@ struct ScanArgs {
     uint64_t n_ftiles;          // filter tiles; n_tiles then counts walk units of kSuper tiles
     unsigned long long* unit_next; // dynamic unit counter (zero at launch)
     uint32_t* tile_region;      // staging region (warp) of each unit
+    const uint32_t* packed;     // symbol-key mode: the text packed by pfac_pack_symbols_kernel, or null
 };
 
 // ---- text and dictionary helpers --------------------------------------------------
@@ -118,6 +119,11 @@ __device__ __forceinline__ uint32_t text_word(const ScanArgs& a, uint64_t pos)
 }
 
 __device__ __forceinline__ uint32_t tail_mask(uint32_t left) { return left >= 4 ? 0xFFFFFFFFu : (1u << (8 * left)) - 1u; }
+// The low min(max(left, 0), 4) bytes of a word.
+__device__ __forceinline__ uint32_t byte_mask(int32_t left)
+{
+    return __funnelshift_lc(0xFFFFFFFFu, 0u, uint32_t(max(left, 0)) * 8u);
+}
 
 // text[start, start + len) == pattern id, 4 bytes per step (patterns are
 // stored 4-byte aligned and zero padded in the image).
@@ -535,6 +541,17 @@ __device__ __forceinline__ bool symbol_key(const ScanArgs& a, const uint16_t* s_
     return ok;
 }
 
+// Symbol-key mode: the start's key read from the packed text (packed word j
+// holds the symbols of bytes [j * 32 / sym_bits, ...), LSB first).
+__device__ __forceinline__ uint32_t packed_key(const ScanArgs& a, uint64_t start)
+{
+    const uint32_t sb = a.trie.sym_bits, kb = sb * a.trie.filter_k;
+    const uint64_t bit = start * sb;
+    const uint32_t* w = a.packed + (bit >> 5);
+    const uint32_t v = __funnelshift_r(__ldg(w), __ldg(w + 1), uint32_t(bit & 31u));
+    return kb >= 32 ? v : v & ((1u << kb) - 1u);
+}
+
 template <int KW>
 __device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
 {
@@ -552,42 +569,74 @@ template <bool PAR>
 __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& h, uint64_t start, uint32_t depth,
                                               Sink& sink)
 {
-    const TrieView& t = a.trie;
     if (h.aux.z & 1u) {
         uint32_t id = h.w.w;
         if (id == kNoId) id = h.aux.w != kNoId ? h.aux.w : resolve_slice<PAR>(a, start, depth);
         if (id == kNoId) atomicOr(a.err, 1u);
         else sink.put(a.g0 + start, depth, id);
     }
-    if (!(h.aux.z & 2u)) return;
-    uint2 span = make_uint2(h.aux.x, h.aux.y);
-    if (t.jump_ext) {
-        // The slot's extension has the first entry and its next 16 bytes:
-        // compare them against the text (an L1 hit next to the window just
-        // read), and touch the pattern only past those 16 bytes.
-        const uint32_t skip = t.depth_limit & ~3u;
-        const uint4* ext = reinterpret_cast<const uint4*>(t.jump_ext) + 2 * h.slot;
-        const uint4 en = __ldg(ext), pv = __ldg(ext + 1);
-        if (start + en.y <= a.n_avail) {
-            const uint64_t p = start + skip;
-            const uint32_t* tw = reinterpret_cast<const uint32_t*>(a.text + (p & ~3ull));
-            const uint32_t sh = uint32_t(p & 3u) * 8u;
-            uint32_t tx[5];
+    if (h.aux.z & 2u) verify_span(a, make_uint2(h.aux.x, h.aux.y), start, sink);
+}
+
+// A slot with an inline pattern list (flags bit 2, layout.hpp): the start's
+// records are exactly the listed patterns that match the text, in list order.
+// Their first 24 bytes from inline_skip came with the extension; the text words are
+// L1 hits next to the window just read.  Pattern bytes are read only past
+// those 24.
+__device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+{
+    const TrieView& t = a.trie;
+    const uint32_t skip = inline_skip(t.filter_k, t.sym_bits);
+    const uint4* ext = reinterpret_cast<const uint4*>(t.jump_ext) + 4 * h.slot;
+    const uint32_t cnt = (h.aux.z >> kJumpInlineShift) & 3u;
+    uint4 x[4];
+    x[0] = __ldg(ext);
+    x[1] = __ldg(ext + 1);
+    x[2] = cnt > 1 ? __ldg(ext + 2) : make_uint4(0u, 0u, 0u, 0u);
+    x[3] = cnt > 1 ? __ldg(ext + 3) : make_uint4(0u, 0u, 0u, 0u);
+    const uint64_t p = start + skip;
+    const uint32_t* tw = reinterpret_cast<const uint32_t*>(a.text + (p & ~3ull));
+    const uint32_t sh = uint32_t(p & 3u) * 8u;
+    uint32_t raw[7], txt[6];
 #pragma unroll
-            for (uint32_t k = 0; k < 5; ++k) tx[k] = __ldg(tw + k); // padded text: safe to overread
-            const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
-            const uint32_t rem = en.y - skip;
-            uint32_t diff = 0;
+    for (uint32_t k = 0; k < 7; ++k) raw[k] = __ldg(tw + k); // padded text: safe to overread
 #pragma unroll
-            for (uint32_t k = 0; k < 4; ++k)
-                if (4 * k < rem) diff |= ((sh ? __funnelshift_r(tx[k], tx[k + 1], sh) : tx[k]) ^ pw[k]) & tail_mask(rem - 4 * k);
-            if (!diff && (rem <= 16 || same_at(a, p + 16, ((uint64_t(en.w) << 32) | en.z) + skip + 16, rem - 16)))
-                sink.put(a.g0 + start, en.y, en.x);
-        }
-        ++span.x;
-        --span.y;
+    for (uint32_t k = 0; k < 6; ++k) txt[k] = sh ? __funnelshift_r(raw[k], raw[k + 1], sh) : raw[k];
+#pragma unroll
+    for (uint32_t j = 0; j < kJumpExtEntries; ++j) {
+        if (j >= cnt) break;
+        const uint4 e0 = x[2 * j], e1 = x[2 * j + 1];
+        const uint32_t id = e0.x, len = e0.y;
+        if (start + len > a.n_avail) continue; // overhangs the text end (scan.cpp:26, :43)
+        const uint32_t pw[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        const int32_t rem = int32_t(len - skip);
+        uint32_t diff = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 6; ++k) diff |= (txt[k] ^ pw[k]) & byte_mask(rem - int32_t(4 * k));
+        if (!diff && (rem <= int32_t(kJumpExtBytes) ||
+                      same_at(a, p + kJumpExtBytes, __ldg(t.pat_off + id) + skip + kJumpExtBytes,
+                              uint32_t(rem) - kJumpExtBytes)))
+            sink.put(a.g0 + start, len, id);
     }
-    verify_span(a, span, start, sink);
+}
+
+// The walking pass (32 warps, 64 registers) keeps the inline check out of
+// line: few of its candidates reach a slot, and inlined it spilled.
+__device__ __noinline__ void emit_inline_call(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+{
+    emit_inline(a, h, start, sink);
+}
+
+template <bool PAR>
+__device__ __forceinline__ void emit_listed(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+{
+#ifndef HFB_INLINE_ALL
+    if (PAR) {
+        emit_inline_call(a, h, start, sink);
+        return;
+    }
+#endif
+    emit_inline(a, h, start, sink);
 }
 
 // A start with more records than the registers hold (rare): walk it again and
@@ -603,7 +652,8 @@ __device__ __noinline__ void rewalk_rest(const ScanArgs& a, const uint16_t* s_sy
     wr.at = at;
     wr.cap = a.warp_cap;
     wr.skip = kRegRecords;
-    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
+    if (hit.aux.z & kJumpInline) emit_listed<PAR>(a, hit, start, wr);
+    else if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
     else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr, hit.aux.w);
 }
 
@@ -652,7 +702,16 @@ struct Walker {
                 start = lo + q[e];
                 win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
                 if (KW != 0 && a.trie.jump_bits) {
-                    if (a.trie.sym_bits) {
+                    if (a.trie.sym_bits && a.packed) {
+                        // the key from the packed text (2 loads, not k symbol
+                        // lookups); bytes outside the alphabet were packed as
+                        // symbol 0, so a hit is checked byte by byte -- by the
+                        // inline compare itself, or here
+                        hit = jump_lookup_key(a.trie, packed_key(a, start), 0u);
+                        uint32_t key;
+                        if (hit.w.z != kNoId && !(hit.aux.z & kJumpInline) && !symbol_key(a, s_sym, start, key))
+                            hit.w.z = kNoId;
+                    } else if (a.trie.sym_bits) {
                         uint32_t key;
                         if (symbol_key(a, s_sym, start, key)) hit = jump_lookup_key(a.trie, key, 0u);
                         else hit.w.z = kNoId;
@@ -663,7 +722,8 @@ struct Walker {
                     depth = a.trie.filter_k;
                 }
                 if (node != kNoId) {
-                    if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
+                    if (hit.aux.z & kJumpInline) emit_listed<PAR>(a, hit, start, sink);
+                    else if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
                     else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink, hit.aux.w);
                 }
             }

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 
 namespace hfb {
@@ -69,13 +70,14 @@ uint32_t ceil_log2(uint64_t x)
 
 // Cuckoo jump table (layout.hpp): entries are 8-word slots whose words 0/1
 // are the key; a slot with word 2 == kNoId is empty.  Grows until every key
-// places (load <= 1/2 to start).  When the walks start at the depth limit
-// (k == limit) and the table stays L2-sized, each slot also gets its
-// extension (layout.hpp kJumpExtWords): the bucket's first entry and that
-// pattern's 16 bytes after the last 4-byte boundary below the limit.
+// places (load <= 1/2 to start).  `lists[i]` (optional) names every pattern
+// with entry i's k-prefix when there are at most kJumpExtEntries of them
+// (flags bit 2, see inline_lists); while the table stays L2-sized those go to
+// the slot's extension (layout.hpp), otherwise bit 2 is cleared.
 using JumpEntry = std::array<uint32_t, kJumpWords>;
+using InlineList = std::array<uint32_t, kJumpExtEntries>;
 
-void build_jump_table(GpuImage& im, const std::vector<JumpEntry>& entries, bool ext)
+void build_jump_table(GpuImage& im, const std::vector<JumpEntry>& entries, const std::vector<InlineList>& lists)
 {
     constexpr size_t W = kJumpWords;
     uint32_t jb = std::max<uint32_t>(ceil_log2(entries.size()) + 1, 4);
@@ -124,24 +126,67 @@ void build_jump_table(GpuImage& im, const std::vector<JumpEntry>& entries, bool 
             im.jump_bits = jb;
             im.jump = std::move(tab);
             im.jump_ext.clear();
-            if (ext && jb <= kMaxJumpExtBits) {
-                const uint32_t skip = im.depth_limit & ~3u;
+            if (!lists.empty() && jb <= kMaxJumpExtBits) {
+                const uint32_t skip = inline_skip(im.filter_k, im.sym_bits);
                 im.jump_ext.assign(kJumpExtWords * slots, 0u);
                 for (size_t s = 0; s < slots; ++s) {
-                    const uint32_t* slot = &im.jump[W * s];
-                    if (where[s] == kNoId || !(slot[6] & 2u)) continue;
-                    uint32_t* x = &im.jump_ext[kJumpExtWords * s];
-                    std::copy_n(&im.bk_entry[4 * size_t(slot[4])], 4, x);
-                    const uint32_t len = x[1];
-                    const uint64_t off = (uint64_t(x[3]) << 32) | x[2];
-                    for (uint32_t b = skip; b < std::min(len, skip + 16); ++b)
-                        x[4 + (b - skip) / 4] |= uint32_t(im.pat_bytes[off + b]) << (8 * ((b - skip) & 3));
+                    if (where[s] == kNoId || !(im.jump[W * s + 6] & kJumpInline)) continue;
+                    const InlineList& l = lists[where[s]];
+                    for (uint32_t j = 0; j < kJumpExtEntries && l[j] != kNoId; ++j) {
+                        uint32_t* x = &im.jump_ext[kJumpExtWords * s + kJumpExtEntryWords * j];
+                        const uint32_t id = l[j], len = im.pat_len[id];
+                        x[0] = id;
+                        x[1] = len;
+                        for (uint32_t b = skip; b < std::min(len, skip + kJumpExtBytes); ++b)
+                            x[2 + (b - skip) / 4] |= uint32_t(im.pat_bytes[im.pat_off[id] + b]) << (8 * ((b - skip) & 3));
+                    }
                 }
+            } else {
+                for (size_t s = 0; s < slots; ++s) im.jump[W * s + 6] &= ~(kJumpInline | (3u << kJumpInlineShift));
             }
             return;
         }
         if (jb > 30) fail(HEPFAC_ERR_NOMEM, "cannot place the jump table");
     }
+}
+
+// Every pattern whose first k bytes (sb == 0) or k packed symbols (sb bits
+// each) give jump key keys[i], sorted by (length, id), when there are at most
+// kJumpExtEntries of them; kNoId-filled otherwise.  For a trie that accepts
+// exactly its dictionary (image.cpp "path ids") these are all the records a
+// start reaching that key can emit, truncated or not, so the walk reduces to
+// verifying them.  Sets flags bit 2 and the count on the entries it fills.
+std::vector<InlineList> inline_lists(const Trie& t, const GpuImage& im, std::vector<JumpEntry>& entries,
+                                     const std::vector<uint64_t>& keys, uint32_t k, uint32_t sb)
+{
+    std::unordered_map<uint64_t, uint32_t> at;
+    at.reserve(keys.size() * 2);
+    for (size_t i = 0; i < keys.size(); ++i) at.emplace(keys[i], uint32_t(i));
+    std::vector<std::vector<uint32_t>> ids(keys.size());
+    for (size_t id = 0; id < t.patterns.size(); ++id) {
+        const auto& p = t.patterns[id];
+        if (p.size() < k) return {}; // cannot happen when k <= min_emit; stay on the walk
+        uint64_t key = 0;
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint8_t c = uint8_t(p[i]);
+            key |= sb ? uint64_t(uint32_t(t.alphabet.symbol_of(c))) << (sb * i) : uint64_t(c) << (8 * i);
+        }
+        auto it = at.find(key);
+        if (it == at.end()) return {}; // a pattern off the trie: not its dictionary
+        if (ids[it->second].size() <= kJumpExtEntries) ids[it->second].push_back(uint32_t(id));
+    }
+    std::vector<InlineList> lists(keys.size());
+    for (size_t i = 0; i < keys.size(); ++i) {
+        lists[i].fill(kNoId);
+        auto& v = ids[i];
+        if (v.empty() || v.size() > kJumpExtEntries) continue;
+        std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
+            return im.pat_len[x] != im.pat_len[y] ? im.pat_len[x] < im.pat_len[y] : x < y;
+        });
+        std::copy(v.begin(), v.end(), lists[i].begin());
+        entries[i][6] |= kJumpInline | (uint32_t(v.size()) << kJumpInlineShift);
+    }
+    return lists;
 }
 
 } // namespace
@@ -293,6 +338,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
         dictionary_language = dictionary_language && order.size() == n && terminal_paths == spelled;
     }
+    im.dictionary_language = dictionary_language;
     im.path_id.assign(n, kKeep);
     if (dictionary_language) {
         for (uint32_t u = 0; u < n; ++u)
@@ -592,7 +638,9 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                                   b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
                                   (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), gram_pend[i]};
                 }
-                build_jump_table(im, entries, opt.jump_ext && im.depth_limit != 0 && im.filter_k == im.depth_limit);
+                std::vector<InlineList> lists;
+                if (opt.jump_ext && im.dictionary_language) lists = inline_lists(t, im, entries, grams, k, 0);
+                build_jump_table(im, entries, lists);
             }
         }
     }
@@ -663,7 +711,10 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                                   b == kNoId ? 0u : im.bk_span[2 * size_t(b) + 1],
                                   (t.terminal(node) ? 1u : 0u) | (b == kNoId ? 0u : 2u), kpend[i]};
                 }
-                build_jump_table(im, entries, opt.jump_ext && im.depth_limit != 0 && im.filter_k == im.depth_limit);
+                std::vector<InlineList> lists;
+                if (opt.jump_ext && im.dictionary_language)
+                    lists = inline_lists(t, im, entries, std::vector<uint64_t>(keys.begin(), keys.end()), ks, sb);
+                build_jump_table(im, entries, lists);
             }
         }
     }

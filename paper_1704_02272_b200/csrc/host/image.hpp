@@ -40,7 +40,8 @@ struct GpuImage {
     std::vector<uint32_t> key4; // pair pipeline: single-probe bitmap over 4-byte path prefixes
     uint32_t jump_bits = 0;     // log2 slots of the depth-k jump table, 0 = none
     std::vector<uint32_t> jump; // uint4 slots, see layout.hpp
-    std::vector<uint32_t> jump_ext; // per slot: first bucket entry + 16 pattern bytes (k == limit), or empty
+    std::vector<uint32_t> jump_ext; // per slot: its inline pattern list (layout.hpp), or empty
+    bool dictionary_language = false; // the trie accepts exactly its patterns (image.cpp "path ids")
 
     uint32_t min_emit = UINT32_MAX; // shortest depth at which any start can report
     uint64_t reach = 0;             // max bytes one start may read; UINT64_MAX = unbounded
@@ -55,7 +56,7 @@ struct ImageOptions {
     uint32_t filter2_slack = 10;   // second level: bits above log2(#k-grams)
     uint32_t max_filter2_bits = 27; // 16 MiB in global memory
     bool jump = true;               // depth-k jump table (HEPFAC_JUMP=0 disables)
-    bool jump_ext = true;           // inline first bucket entries in the jump table (HEPFAC_JUMP_EXT=0 disables)
+    bool jump_ext = true;           // inline pattern lists in the jump table (HEPFAC_JUMP_EXT=0 disables)
     uint32_t filter_mode = 0;       // 0 = cost model, 1 = single, 2 = pair (HEPFAC_FILTER_MODE)
     bool lean_single = false;       // selective single-probe tries on the two-pass pipeline (HEPFAC_LEAN_SINGLE)
     bool symbol_keys = true;        // packed-symbol filter keys for sigma <= 16 (HEPFAC_SYMBOL_KEYS=0 disables)
