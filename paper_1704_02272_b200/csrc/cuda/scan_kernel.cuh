@@ -119,6 +119,19 @@ __device__ __forceinline__ uint32_t text_word(const ScanArgs& a, uint64_t pos)
 }
 
 __device__ __forceinline__ uint32_t tail_mask(uint32_t left) { return left >= 4 ? 0xFFFFFFFFu : (1u << (8 * left)) - 1u; }
+// The aligned words holding text[start, start + 8), and that window from them.
+__device__ __forceinline__ uint3 raw_window(const ScanArgs& a, uint64_t start)
+{
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(a.text + (start & ~3ull));
+    return make_uint3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+}
+__device__ __forceinline__ uint64_t window_of(uint3 w, uint64_t start)
+{
+    const uint32_t sh = uint32_t(start & 3u) * 8u;
+    const uint32_t lo = sh ? __funnelshift_r(w.x, w.y, sh) : w.x, hi = sh ? __funnelshift_r(w.y, w.z, sh) : w.y;
+    return (uint64_t(hi) << 32) | lo;
+}
+
 // The low min(max(left, 0), 4) bytes of a word.
 __device__ __forceinline__ uint32_t byte_mask(int32_t left)
 {
@@ -688,8 +701,16 @@ struct Walker {
             }
             __syncwarp();
         }
+        // The fused kernel loads each round's text windows one round ahead,
+        // so a candidate's jump lookup does not wait for its text (c2 +2.5%;
+        // the walking pass, at 64 registers, lost 1-3% with it).
+        uint3 pre = make_uint3(0u, 0u, 0u);
+        if (!PAR && lane < ns) pre = raw_window(a, lo + q[lane]);
         for (uint32_t r0 = 0; r0 < ns; r0 += 32) {
             const uint32_t e = r0 + lane;
+            uint3 cur = pre;
+            if (!PAR && e + 32 < ns) pre = raw_window(a, lo + q[e + 32]);
+            if (PAR && e < ns) cur = raw_window(a, lo + q[e]);
             Sink sink;
             uint64_t start = 0;
             uint64_t win = 0;
@@ -700,7 +721,7 @@ struct Walker {
             const bool at_limit = KW != 0 && a.trie.jump_bits && a.trie.filter_k == a.trie.depth_limit;
             if (e < ns) {
                 start = lo + q[e];
-                win = (uint64_t(text_word(a, start + 4)) << 32) | text_word(a, start);
+                win = window_of(cur, start);
                 if (KW != 0 && a.trie.jump_bits) {
                     if (a.trie.sym_bits && a.packed) {
                         // the key from the packed text (2 loads, not k symbol
