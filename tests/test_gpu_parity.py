@@ -419,6 +419,43 @@ def test_symbol_key_mode(gpu, sigma):
             assert same(gpu.scan(t, tx), want), (sigma, n, t.stage(), t.depth_limit())
 
 
+@pytest.mark.parametrize("sigma", [2, 4])
+def test_symbol_key_aliased_bytes(gpu, sigma):
+    # Bytes outside the alphabet pack as symbol 0, so a start whose first k
+    # bytes hold one can produce a real jump key.  The walk must still reject
+    # it: inline lists by comparing bytes from byte 0, longer lists (several
+    # patterns sharing the key) by the byte-wise symbol check.  Patterns up to
+    # 40 bytes also take the inline compare past its 24 stored bytes.
+    rng = np.random.default_rng(90 + sigma)
+    a, syms = alphabet_bytes(gpu, sigma)
+    pats = set(pattern_set(rng, syms, 300, 17, 40))
+    for _ in range(20):  # keys shared by 3-5 patterns
+        head = bytes(syms[rng.integers(0, syms.size, size=16)])
+        for _ in range(int(rng.integers(3, 6))):
+            pats.add(head + bytes(syms[rng.integers(0, syms.size, size=int(rng.integers(1, 20)))]))
+    pats = sorted(pats)
+    full = build(gpu, pats, sigma)
+    assert gpu.layout_info(full)["filter_mode"] == 3
+    s1, _ = full.compress(1)
+    tries = [full, s1, full.compress(2)[0], s1.truncate(16)[0]]
+    tx = text(rng, syms, 1 << 18)
+    at = 0
+    for p in pats:
+        for bad in (0xFF, 0x00):
+            q = bytearray(p)
+            zeros = [j for j in range(min(16, len(q))) if q[j] == syms[0]]
+            if zeros:
+                q[zeros[int(rng.integers(0, len(zeros)))]] = bad
+            plant(tx, bytes(q), at)
+            at += len(q) + 3
+        plant(tx, p, at)
+        at += len(p) + 3
+    assert at < tx.size
+    want = oracle.naive_find_all(tx, pats)
+    for t in tries:
+        assert same(gpu.scan(t, tx), want), (sigma, t.stage(), t.depth_limit())
+
+
 def test_symbol_key_mode_streamed(gpu, monkeypatch):
     rng = np.random.default_rng(77)
     a, syms = alphabet_bytes(gpu, 4)
