@@ -529,3 +529,44 @@ def test_multi_device_scan(gpu, monkeypatch, devices):
     monkeypatch.setenv("HEPFAC_DEVICES", "9")
     with pytest.raises(H.HepfacError):
         gpu.scan(t, tx)
+
+
+def test_concurrent_scans_share_one_trie(gpu):
+    # hepfac.h:4-8 / SURVEY 8(b): handles are shared read-only across threads
+    # and hepfac_scan may run concurrently on one trie (ctypes drops the GIL
+    # during the call).  Eight threads, two tries (one truncated, so both
+    # kernel paths and both jump-table forms run at once), distinct texts.
+    import threading
+
+    rng = np.random.default_rng(123)
+    a, syms = alphabet_bytes(gpu, 256)
+    pats = pattern_set(rng, syms, 500, 4, 20)
+    full = build(gpu, pats, 256, 2)
+    trunc = build(gpu, pats, 256, 1, 4)
+    texts = []
+    for i in range(8):
+        tx = text(rng, syms, int(rng.integers(1 << 16, 1 << 20)))
+        for j in range(0, tx.size - 32, 997):
+            plant(tx, pats[(i * 31 + j) % len(pats)], j)
+        texts.append(tx)
+    wants = [oracle.naive_find_all(tx, pats) for tx in texts]
+    results, errors = [None] * 8, []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                got = gpu.scan(full if i % 2 else trunc, texts[i])
+                if not same(got, wants[i]):
+                    results[i] = False
+                    return
+            results[i] = True
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    assert all(results), results
