@@ -73,6 +73,37 @@ def test_error_codes(lib):
     assert e.value.status == H.STATE
 
 
+def test_last_error_is_thread_local(lib):
+    # capi.cpp:37, 138-141: each thread reads the message of its own last
+    # failure, whatever other threads did in between.
+    import threading
+
+    a = lib.alphabet(4)
+    step = threading.Barrier(2)
+    seen = {}
+
+    def first():
+        assert lib.dll.hepfac_trie_build(None, None) == H.INVALID_ARG
+        step.wait()  # the other thread fails differently
+        step.wait()
+        seen["first"] = lib.last_error()
+
+    def second():
+        step.wait()
+        with pytest.raises(H.HepfacError):
+            lib.patterns([b"AB"], a)
+        seen["second"] = lib.last_error()
+        step.wait()
+
+    ts = [threading.Thread(target=first), threading.Thread(target=second)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert seen["first"] == "null argument"
+    assert "0x42" in seen["second"]
+
+
 def test_out_untouched_on_failure(lib):
     import ctypes as C
     a = lib.alphabet(4)
