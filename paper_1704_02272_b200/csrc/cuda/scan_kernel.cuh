@@ -1071,13 +1071,26 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
     grid.sync();
 
     // phase 3: scan the chunk, copy staged slices to their final offsets
-    const unsigned long long origin = *a.base_in;
-    unsigned long long base = origin, total = 0;
-    for (uint32_t b = 0; b < gridDim.x; ++b) {
-        const unsigned long long v = a.chunk_sum[b];
-        base += b < blockIdx.x ? v : 0ull;
-        total += v;
+    // warp 0 sums the CTA sums (before this CTA, and all) for the whole CTA
+    __shared__ unsigned long long s_base[2];
+    if (warp == 0) {
+        unsigned long long before = 0, all = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            const unsigned long long v = a.chunk_sum[b];
+            before += b < blockIdx.x ? v : 0ull;
+            all += v;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            before += __shfl_xor_sync(0xFFFFFFFFu, before, d);
+            all += __shfl_xor_sync(0xFFFFFFFFu, all, d);
+        }
+        if (lane == 0) s_base[0] = before, s_base[1] = all;
     }
+    __syncthreads();
+    const unsigned long long origin = *a.base_in;
+    unsigned long long base = origin + s_base[0];
+    const unsigned long long total = s_base[1];
     if (blockIdx.x == gridDim.x - 1 && tid == 0) {
         *a.total = total;
         *a.base_out = origin + total;
@@ -1092,6 +1105,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
             const uint64_t region = CANDS ? a.tile_region[i] : i % (uint64_t(gridDim.x) * NW);
             const uint4* src = reinterpret_cast<const uint4*>(a.stage + region * a.warp_cap) + a.tile_slot[i];
             uint4* dst = reinterpret_cast<uint4*>(a.out) + base + ex;
+#pragma unroll 4
             for (uint32_t k = 0; k < n; ++k) dst[k] = src[k];
         }
         base += tot;
