@@ -136,8 +136,15 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
 #pragma unroll
             for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
             if (s + 1 < steps) {
+                const uint64_t nb = sbase + kFStep;
+                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
+                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
 #pragma unroll
-                for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(sbase + kFStep + b * kFChunk);
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
+                } else {
+#pragma unroll
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
+                }
             }
             // lane 31's overhang of the last chunk: the first word after the step
             uint32_t tail = 0;
@@ -320,8 +327,15 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_single_filter_kernel(const 
 #pragma unroll
             for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
             if (s + 1 < steps) {
+                const uint64_t nb = sbase + kFStep;
+                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
+                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
 #pragma unroll
-                for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(sbase + kFStep + b * kFChunk);
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
+                } else {
+#pragma unroll
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
+                }
             }
             uint2 tail = make_uint2(0u, 0u); // lane 31's overhang of the last chunk
             if (lane == 31 && sbase + kFStep < avail16)
