@@ -232,7 +232,6 @@ def main():
 
     from paper_1704_02272_b200 import hepfac, workloads
 
-    d = Dist(args.gpus)
     w = workloads.config(args.config, sigma=args.sigma, count=args.count)
     workload_desc = {
         "c1": "1,000 byte patterns len 4-32 over synthetic payload",
@@ -244,8 +243,8 @@ def main():
 
     if args.impl == "reference":
         # Reference arm: rank 0 only, CPU, bounded sample of the same workload.
-        if d.rank != 0:
-            d.close()
+        # No process group and no CUDA context: the other ranks exit at once.
+        if int(os.environ.get("RANK", "0")) != 0:
             return
         sample = w.make_text(args.cpu_sample_bytes)
         times = []
@@ -278,6 +277,7 @@ def main():
         }))
         return
 
+    d = Dist(args.gpus)
     lib = hepfac.lib()
     if lib.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device")

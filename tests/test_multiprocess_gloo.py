@@ -95,3 +95,26 @@ def test_plan_covers_every_start_once():
             assert all(s.end == min(n, s.lo + s.owned + 31) for s in shards)
     with pytest.raises(ValueError):
         D.plan(10, 2, 0, -1)
+
+
+def test_reference_arm_under_torchrun():
+    # The driver launches `bench.py --impl reference` like the GPU arm
+    # (torchrun, N ranks): rank 0 times the compiled reference on the CPU and
+    # prints one JSON line; the other ranks exit 0 without a process group or
+    # a CUDA context (this container has no GPU).
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--cpu-sample-bytes", str(2 << 20)]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    if "unavailable" not in line:
+        assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+        assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
