@@ -479,9 +479,16 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_symbol_filter_kernel(const 
         const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
         const uint32_t chunks = (rem + kChunk - 1) / kChunk;
         const uint64_t w0 = lo / kPer; // first packed word of the tile
+        // each chunk's two words load one chunk ahead (padded array)
+        uint32_t n0 = 0, n1 = 0;
+        if (chunks) n0 = __ldg(packed + w0 + lane), n1 = __ldg(packed + w0 + lane + 1);
         for (uint32_t c = 0; c < chunks; ++c) {
-            const uint64_t wi = w0 + uint64_t(c) * 32 + lane;
-            const uint32_t a0 = __ldg(packed + wi), a1 = __ldg(packed + wi + 1); // padded array
+            const uint32_t a0 = n0, a1 = n1;
+            if (c + 1 < chunks) {
+                const uint64_t wn = w0 + uint64_t(c + 1) * 32 + lane;
+                n0 = __ldg(packed + wn);
+                n1 = __ldg(packed + wn + 1);
+            }
             uint32_t m0 = 0, m1 = 0;
 #pragma unroll
             for (uint32_t j = 0; j < kPer; ++j) {
