@@ -915,8 +915,11 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                         const uint64_t at = (t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i);
                         v = uint16_t(a.cand[at] + i * kTile);
                         keep = true;
-                        if (fwords) { // no prefix bitmap in symbol-key mode
-                            const uint32_t key = a.cand_key[at];
+                        if (fwords) {
+                            // symbol keys are re-hashed: the filter pass
+                            // already used this hash of the same key
+                            uint32_t key = a.cand_key[at];
+                            if (a.trie.sym_bits) key = filter2_hash(key);
                             const uint32_t word =
                                 *reinterpret_cast<const uint32_t*>(kbytes + (__umulhi(key, kFilterMul) & kmask4));
                             keep = int32_t(word << (key & 31u)) < 0;

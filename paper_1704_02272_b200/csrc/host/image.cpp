@@ -700,7 +700,21 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 im.filter_pass = double(set) / double(uint64_t(1) << bits);
                 im.filter2_bits = 0;
                 im.filter2.clear();
+                // the walking pass re-checks candidates' packed keys under an
+                // independent hash (filter2_hash first), like key4 for bytes,
+                // when most filter survivors of random text would be false
+                // positives (c4 sigma=4: +28%; sigma=2, where a random key is
+                // a real path as often as a false positive, lost 3%)
                 im.key4.clear();
+                const double p_true = double(keys.size()) / std::ldexp(1.0, int(sb * ks));
+                if (p_true < 0.25 * im.filter_pass) {
+                    const uint32_t kb = std::clamp<uint32_t>(ceil_log2(keys.size()) + opt.filter_slack, 10, 20);
+                    im.key4.assign((size_t(1) << kb) / 32, 0u);
+                    for (uint32_t key : keys) {
+                        const uint32_t h = filter2_hash(key);
+                        im.key4[filter_word(h, kb - 5)] |= filter_mask_bit(h);
+                    }
+                }
                 im.lean_single = false;
                 std::vector<JumpEntry> entries(keys.size());
                 for (size_t i = 0; i < keys.size(); ++i) {
