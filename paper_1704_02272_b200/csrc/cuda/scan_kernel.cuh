@@ -723,7 +723,8 @@ struct Walker {
                 start = lo + q[e];
                 win = window_of(cur, start);
                 if (KW != 0 && a.trie.jump_bits) {
-                    if (a.trie.sym_bits && a.packed) {
+                    // (grouped records mean sigma > 32: never symbol keys)
+                    if (!GROUPED && a.trie.sym_bits && a.packed) {
                         // the key from the packed text (2 loads, not k symbol
                         // lookups); bytes outside the alphabet were packed as
                         // symbol 0, so a hit is checked byte by byte -- by the
@@ -732,7 +733,7 @@ struct Walker {
                         uint32_t key;
                         if (hit.w.z != kNoId && !(hit.aux.z & kJumpInline) && !symbol_key(a, s_sym, start, key))
                             hit.w.z = kNoId;
-                    } else if (a.trie.sym_bits) {
+                    } else if (!GROUPED && a.trie.sym_bits) {
                         uint32_t key;
                         if (symbol_key(a, s_sym, start, key)) hit = jump_lookup_key(a.trie, key, 0u);
                         else hit.w.z = kNoId;
@@ -919,7 +920,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                             // symbol keys are re-hashed: the filter pass
                             // already used this hash of the same key
                             uint32_t key = a.cand_key[at];
-                            if (a.trie.sym_bits) key = filter2_hash(key);
+                            if (!GROUPED && a.trie.sym_bits) key = filter2_hash(key);
                             const uint32_t word =
                                 *reinterpret_cast<const uint32_t*>(kbytes + (__umulhi(key, kFilterMul) & kmask4));
                             keep = int32_t(word << (key & 31u)) < 0;
