@@ -274,7 +274,7 @@ __device__ __forceinline__ uint32_t f_single_level1(const uint32_t (&w)[6], uint
         if (KW == 2) {
             const uint32_t hi =
                 ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
-            key = lo ^ (hi * 0x85EBCA77u); // filter_fold
+            key = lo + hi * 0x85EBCA77u; // filter_fold
         }
         const uint32_t word = f_lds(tbase + (__umulhi(key, kFilterMul) & mask4)); // filter_word(key) * 4
         uint32_t& m = j < 8 ? m0 : m1;

@@ -364,7 +364,7 @@ __device__ __forceinline__ uint32_t filter_mask(const TrieView& t, const uint32_
         if (KW == 2) {
             const uint32_t hi =
                 ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
-            key = lo ^ (hi * 0x85EBCA77u); // filter_fold
+            key = lo + hi * 0x85EBCA77u; // filter_fold (one IMAD)
         } else {
             key = KW == 3 ? lo : (lo & m32);
         }
@@ -497,7 +497,7 @@ __device__ __forceinline__ bool probe2(const ScanArgs& a, uint64_t start)
     if (KW == 1) key &= (1u << (8 * k)) - 1u;
     if (KW == 2) {
         const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : ((1u << (8 * (k - 4))) - 1u);
-        key ^= (text_word(a, start + 4) & mhi) * 0x85EBCA77u; // filter_fold
+        key += (text_word(a, start + 4) & mhi) * 0x85EBCA77u; // filter_fold
     }
     const uint32_t slot = filter2_slot(key, t.filter2_bits);
     return (__ldg(t.filter2 + (slot >> 5)) >> (slot & 31u)) & 1u;
