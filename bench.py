@@ -180,13 +180,26 @@ def ncu_traffic(config_name: str, text_bytes: int):
 
 
 def make_shard(w, rank: int, world: int, per_gpu: int, halo: int):
-    """Rank r owns global starts [r*per_gpu, (r+1)*per_gpu) and gets `halo`
-    extra bytes of right context."""
+    """Rank r owns global starts [r*per_gpu, (r+1)*per_gpu) of one global
+    text of world*per_gpu bytes and gets the `halo` bytes after them -- the
+    next rank's first bytes."""
     N = per_gpu * world
     lo = rank * per_gpu
     end = min(N, lo + per_gpu + halo)
-    text = w.make_text(end - lo, offset_seed=rank)
+    text = w.make_text(end - lo, lo=lo)
     return text, lo, per_gpu
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_reference_gbps(w, trie_state: str, sample: np.ndarray, runs: int = 3):
@@ -228,6 +241,8 @@ def main():
     ap.add_argument("--cpu-sample-bytes", type=int, default=256 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
+    ap.add_argument("--check", action="store_true",
+                    help="compare the rank-order concatenation of the shard lists with a one-rank scan (SHA-256)")
     args = ap.parse_args()
 
     from paper_1704_02272_b200 import hepfac, workloads
@@ -246,7 +261,6 @@ def main():
         # No process group and no CUDA context: the other ranks exit at once.
         if int(os.environ.get("RANK", "0")) != 0:
             return
-        sample = w.make_text(args.cpu_sample_bytes)
         times = []
         import oracle
         ref = oracle.ref_library()
@@ -256,6 +270,7 @@ def main():
             print(json.dumps(out))
             return
         t, _ = workloads.build_trie(ref, w, args.trie)
+        sample = w.make_text(args.cpu_sample_bytes)
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             res = ref.scan(t, sample, workers=cores)
@@ -271,6 +286,7 @@ def main():
             "data": "synthetic", "config": {"workload": f"{args.config}: {workload_desc}", "trie": args.trie,
                                             "sample_bytes": int(sample.size), "matches": int(res.size)},
             "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+                             "cpu_model": cpu_model(),
                              "sample": f"{sample.size >> 20} MiB of the {args.config} text, hepfac_scan "
                                        f"(walk + merge + sort), {cores} workers"},
             "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -308,7 +324,11 @@ def main():
     mean_launch_s = total_ms / args.steps / 1e3
     sess.close()
 
-    # ---- e2e: hepfac_scan on pinned host memory --------------------------
+    # ---- e2e: hepfac_scan from host memory ---------------------------------
+    # pinned (the config-3 contract: "streamed from pinned host memory") and
+    # pageable (the reference's normal caller: a std::vector, staged by the
+    # library through its pinned ring); H2D, kernels, per-chunk D2H of the
+    # sorted list and the count exchange all inside the timed region
     try:
         import torch
         pinned = torch.empty(text.size, dtype=torch.uint8, pin_memory=True)
@@ -317,25 +337,73 @@ def main():
     except Exception:
         host = text
     e2e_steps = args.e2e_steps or min(args.steps, 5)
-    for _ in range(min(args.warmup, 2)):
-        res = lib.scan_shard(trie, host, lo, owned)
-    d.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        res = lib.scan_shard(trie, host, lo, owned)
-        _prefix = d.exclusive_prefix(int(res.size))
-    d.barrier()
-    e2e_s = d.max(time.perf_counter() - t0)
-    stats = lib.last_scan_stats()
+
+    def e2e_run(buf):
+        for _ in range(min(args.warmup, 2)):
+            r = lib.scan_shard(trie, buf, lo, owned)
+        d.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            r = lib.scan_shard(trie, buf, lo, owned)
+            d.exclusive_prefix(int(r.size))
+        d.barrier()
+        return r, d.max(time.perf_counter() - t0), lib.last_scan_stats()
+
+    res, e2e_s, stats = e2e_run(host)
     e2e_val = gbps(all_bytes * e2e_steps, e2e_s)
     total_matches = d.sum(int(res.size))
+    # the host-link ceiling: a plain pinned H2D copy of up to 1 GiB (torch)
+    h2d_ceiling = None
+    try:
+        import torch
+        n = min(text.size, 1 << 30)
+        dev = torch.empty(n, dtype=torch.uint8, device="cuda")
+        src = pinned[:n]
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dev.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        h2d_ceiling = gbps(n, best / 1e3)
+        del dev
+    except Exception:
+        pass
+    res_pg, e2e_pg_s, stats_pg = e2e_run(text)
+    e2e_pg_val = gbps(all_bytes * e2e_steps, e2e_pg_s)
+    if not (res_pg.shape == res.shape and (res_pg == res).all()):
+        raise SystemExit("pageable and pinned hepfac_scan results differ")
+
+    # ---- --check: the rank-order concatenation equals a one-rank scan ---------
+    check = None
+    if args.check:
+        import hashlib
+        parts = [res.tobytes()]
+        if d.pg:
+            parts = [None] * d.world
+            d.pg.all_gather_object(parts, res.tobytes())
+        if d.rank == 0:
+            mine = hashlib.sha256(b"".join(parts)).hexdigest()
+            whole = w.make_text(owned * d.world)
+            one = lib.scan(trie, whole)
+            ref_sha = hashlib.sha256(one.tobytes()).hexdigest()
+            check = {"equal": mine == ref_sha, "sha256": mine, "one_rank_sha256": ref_sha,
+                     "matches": int(one.size), "global_bytes": int(whole.size),
+                     "how": "SHA-256 of the rank-order concatenation of every rank's hepfac_b200_scan_shard list "
+                            "vs hepfac_scan of the whole global text on one device"}
+            if not check["equal"]:
+                print(json.dumps({"check": check}), file=sys.stderr)
+        d.barrier()
 
     # ---- roofline of the dominant kernel ----------------------------------------
     # Pair pipeline: the filter pass reads the text (1 B per start) and is the
     # dominant kernel; the walking pass writes the records (16 B per match).
     # Fused kernel: both in one launch.
     peak, peak_src = measured_hbm_peak()
-    pipeline = kernels_per_scan == 2
+    pipeline = kernels_per_scan >= 2
     first_s = sum(first_ms) / len(first_ms) / 1e3
     second_s = sum(second_ms) / len(second_ms) / 1e3
     alg_bytes = owned if pipeline else owned + 16 * int(matches)
@@ -343,7 +411,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config, owned),
                 "peak_source": peak_src,
-                "kernel": "pfac_pair_filter_kernel (filter pass)" if pipeline else "pfac_scan_kernel (fused)",
+                "kernel": ({2: "pfac_pair_filter_kernel (filter pass)",
+                            3: "pfac_pack_symbols_kernel + pfac_symbol_filter_kernel (filter pass)"}
+                           .get(kernels_per_scan, "pfac_scan_kernel (fused)")),
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "per_unit": "1 B text read per start" + ("" if pipeline else " + 16 B per match written"),
                 "step_share": round(first_s / mean_launch_s, 4)}
@@ -361,9 +431,17 @@ def main():
                    f"{halo} B halo)", "l2": l2_note, "matches_per_gpu": int(matches),
                    "filter": {"k": info["filter_k"], "bits": info["filter_bits"], "paths": info["filter_paths"]}},
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": int(text.size),
-                "d2h_bytes_per_step": int(res.size) * 16, "steps": e2e_steps,
+                "d2h_bytes_per_step": int(res.size) * 16, "steps": e2e_steps, "host_memory": "pinned",
                 "device_breakdown_ms": {k: round(stats[k], 3) for k in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")},
-                "matches_total": total_matches},
+                "chunks": stats["chunks"], "matches_total": total_matches,
+                "h2d_ceiling_Gbps": round(h2d_ceiling, 1) if h2d_ceiling else None},
+        "e2e_pageable": {"value": round(e2e_pg_val, 3), "unit": UNIT, "h2d_bytes_per_step": int(text.size),
+                         "d2h_bytes_per_step": int(res_pg.size) * 16, "steps": e2e_steps,
+                         "host_memory": "pageable (numpy), staged by the library through its pinned ring",
+                         "staged": bool(stats_pg["staged"]),
+                         "device_breakdown_ms": {k: round(stats_pg[k], 3)
+                                                 for k in ("h2d_ms", "kernel_ms", "d2h_ms", "total_ms")},
+                         "vs_pinned": round(e2e_pg_val / e2e_val, 4) if e2e_val else None},
         "gpu_launches": args.steps * kernels_per_scan,
         "roofline": roofline,
         "kernels": kernels,
@@ -375,6 +453,7 @@ def main():
         sample = np.ascontiguousarray(text[: min(args.cpu_sample_bytes, text.size)])
         g, cores, kind, rep = cpu_reference_gbps(w, args.trie, sample)
         out["cpu_baseline"] = {"value": round(g, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                               "cpu_model": cpu_model(),
                                "sample": f"first {sample.size >> 20} MiB of the same text; "
                                          f"hepfac_run_throughput walk-phase mean of 3 runs after 1 warm-up"}
         if "single_worker" in rep:
@@ -382,9 +461,13 @@ def main():
             out["cpu_baseline"]["single_worker"] = {
                 "value": sw["value"], "unit": UNIT, "cores": 1,
                 "sample": f"first {sw['sample_bytes'] >> 20} MiB of the same text, same timing"}
+    if check is not None:
+        out["check"] = check
     if d.rank == 0:
         print(json.dumps(out))
     d.close()
+    if check is not None and not check["equal"]:
+        raise SystemExit(1)
 
 
 if __name__ == "__main__":

@@ -44,9 +44,16 @@ typedef struct hepfac_b200_scan_stats {
     uint32_t chunks;
     uint32_t relaunches;
     int32_t device;
+    uint32_t staged;   /* 1: the text was pageable and went through the pinned staging ring */
 } hepfac_b200_scan_stats_t;
 
 hepfac_status_t hepfac_b200_last_scan_stats(hepfac_b200_scan_stats_t* out);
+
+/* Frees every pooled per-call workspace (device buffers, streams) and pooled
+ * pinned host block that no call is using.  Calls after it re-allocate on
+ * demand.  Pooled workspaces otherwise keep at most HEPFAC_POOL_KEEP_MIB
+ * (default 2048) MiB of device buffers each between calls. */
+hepfac_status_t hepfac_b200_trim(void);
 
 /* Device-resident session: text uploaded once, scanned repeatedly.  Same
  * shard convention as hepfac_b200_scan_shard (offset = 0, owned = bytes for a
@@ -62,7 +69,9 @@ hepfac_status_t hepfac_b200_session_run(hepfac_b200_session_t* session, uint32_t
 /* Per-kernel device times of the last run's scans (CUDA events on the
  * engine's stream): first = the filter pass of the pair pipeline, or the fused
  * scan kernel; second = the candidate-walking pass (0 when there is none).
- * *kernels_per_scan (may be NULL) = kernel launches per scan (1 or 2). */
+ * *kernels_per_scan (may be NULL) = kernel launches per scan: 1 (fused), 2
+ * (filter + walking pass) or 3 (symbol packing + filter + walking pass; the
+ * packing pass is timed with the filter pass). */
 hepfac_status_t hepfac_b200_session_kernel_ms(hepfac_b200_session_t* session, uint32_t iterations,
                                               double* first_ms, double* second_ms, uint32_t* kernels_per_scan);
 /* Copies the last run's sorted matches to the host. */

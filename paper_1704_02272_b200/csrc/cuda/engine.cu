@@ -6,7 +6,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -69,6 +73,23 @@ int pick_device()
     return d;
 }
 
+// Dynamic shared memory is a per-kernel-function attribute, and every trie
+// with the same kernel choice shares one instantiation, so a per-trie size
+// would let a small trie lower the cap below what a bigger trie's launch
+// needs.  The cap is set once to the device's opt-in maximum instead (the
+// value is the same for every caller, so concurrent setters cannot race it
+// down); each launch still passes its own trie's size.
+template <typename F>
+void allow_max_smem(F* fn, int device)
+{
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)));
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            optin - int(fa.sharedSizeBytes)));
+}
+
 template <typename T>
 T* dev_alloc(size_t count)
 {
@@ -90,18 +111,140 @@ int device_count()
 }
 
 // ---------------------------------------------------------------------------
+// Pinned host memory: match lists and staging buffers are page-locked so the
+// D2H of records (and the H2D of staged text) run at PCIe speed and overlap
+// the kernels.  cudaHostAlloc costs far more than malloc, so freed blocks are
+// kept in a small process-wide pool (HEPFAC_PINNED_POOL_MIB, default 1024 MiB
+// of free blocks) and reused by later calls.
+
+namespace {
+
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<size_t, void*>> free; // (capacity, block)
+    size_t free_bytes = 0;
+
+    static size_t keep_limit()
+    {
+        size_t mib = 1024;
+        if (const char* s = std::getenv("HEPFAC_PINNED_POOL_MIB")) mib = size_t(std::strtoull(s, nullptr, 10));
+        return mib << 20;
+    }
+    // A block of at least `bytes` (capacities are powers of two >= 1 MiB).
+    std::pair<void*, size_t> acquire(size_t bytes)
+    {
+        size_t cap = size_t(1) << 20;
+        while (cap < bytes) cap <<= 1;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            size_t best = free.size();
+            for (size_t i = 0; i < free.size(); ++i)
+                if (free[i].first >= cap && (best == free.size() || free[i].first < free[best].first)) best = i;
+            if (best != free.size()) {
+                auto b = free[best];
+                free.erase(free.begin() + long(best));
+                free_bytes -= b.first;
+                return {b.second, b.first};
+            }
+        }
+        void* p = nullptr;
+        const cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            trim(0); // give the pool's blocks back and retry once
+            if (cudaHostAlloc(&p, cap, cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                throw std::bad_alloc();
+            }
+        }
+        return {p, cap};
+    }
+    void release(void* p, size_t cap)
+    {
+        if (!p) return;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (free_bytes + cap <= keep_limit()) {
+                free.emplace_back(cap, p);
+                free_bytes += cap;
+                return;
+            }
+        }
+        cudaFreeHost(p);
+    }
+    void trim(size_t keep)
+    {
+        std::vector<std::pair<size_t, void*>> drop;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            while (!free.empty() && free_bytes > keep) {
+                drop.push_back(free.back());
+                free_bytes -= free.back().first;
+                free.pop_back();
+            }
+        }
+        for (auto& b : drop) cudaFreeHost(b.second);
+    }
+};
+
+PinnedPool& pinned_pool()
+{
+    static PinnedPool* p = new PinnedPool; // never destroyed: lists may outlive static destructors
+    return *p;
+}
+
+// Lists up to this many bytes live in ordinary heap memory.
+constexpr size_t kPinnedListMin = size_t(1) << 20;
+
+} // namespace
+
+// ---------------------------------------------------------------------------
 // MatchList
 
-MatchList::~MatchList() { std::free(data); }
+MatchList::~MatchList() { release(); }
+
+void MatchList::release()
+{
+    if (pinned) pinned_pool().release(data, cap * sizeof(hepfac_match_t));
+    else std::free(data);
+    data = nullptr;
+    cap = 0;
+    pinned = false;
+}
 
 void MatchList::allocate(size_t n)
 {
-    std::free(data);
-    data = nullptr;
+    release();
     size = n;
     if (n == 0) return;
-    data = static_cast<hepfac_match_t*>(std::malloc(n * sizeof(hepfac_match_t)));
-    if (!data) throw std::bad_alloc();
+    reserve(n);
+}
+
+void MatchList::reserve(size_t n)
+{
+    if (n <= cap) return;
+    hepfac_match_t* old = data;
+    const bool old_pinned = pinned;
+    const size_t old_cap = cap;
+    if (n * sizeof(hepfac_match_t) >= kPinnedListMin) {
+        auto b = pinned_pool().acquire(n * sizeof(hepfac_match_t));
+        data = static_cast<hepfac_match_t*>(b.first);
+        cap = b.second / sizeof(hepfac_match_t);
+        pinned = true;
+    } else {
+        data = static_cast<hepfac_match_t*>(std::malloc(n * sizeof(hepfac_match_t)));
+        if (!data) {
+            data = old;
+            throw std::bad_alloc();
+        }
+        cap = n;
+        pinned = false;
+    }
+    if (old) {
+        if (size) std::memcpy(data, old, std::min(size, old_cap) * sizeof(hepfac_match_t));
+        if (old_pinned) pinned_pool().release(old, old_cap * sizeof(hepfac_match_t));
+        else std::free(old);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -161,6 +304,13 @@ namespace {
 bool pair_pipeline_enabled()
 {
     const char* s = std::getenv("HEPFAC_PAIR_PIPELINE");
+    return !s || std::strtol(s, nullptr, 10) != 0;
+}
+
+// HEPFAC_PAIR_QUEUE=0: the in-lane form of the pair filter pass (A/B only).
+bool pair_queue_form()
+{
+    const char* s = std::getenv("HEPFAC_PAIR_QUEUE");
     return !s || std::strtol(s, nullptr, 10) != 0;
 }
 
@@ -260,7 +410,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     // one-pass (fused) kernel: always available
     d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
     d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
-    CK(cudaFuncSetAttribute(d->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->smem)));
+    allow_max_smem(d->kernel, device);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     // two-pass pipeline (always for symbol keys: the one-pass kernel reads byte keys)
@@ -276,24 +426,30 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                                           : (im.sym_bits == 2 ? gpu::pfac_pack_symbols_kernel<2>
                                                               : gpu::pfac_pack_symbols_kernel<4>);
         } else {
-            d->filter_fn = !d->lean_single ? gpu::pfac_pair_filter_kernel
+            d->filter_fn = !d->lean_single ? (pair_queue_form() ? gpu::pfac_pair_filter_kernel
+                                                                : gpu::pfac_pair_filter2_kernel)
                                            : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3>
                                                          : gpu::pfac_single_filter_kernel<2>);
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
-        CK(cudaFuncSetAttribute(d->walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->walk_smem)));
+        allow_max_smem(d->walk_kernel, device);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->walk_blocks_per_sm, d->walk_kernel,
                                                          int(gpu::kCWarps * 32), d->walk_smem));
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         d->filter_smem = size_t(v.filter_words) * 4 +
-                         ((d->lean_single || im.filter_mode == 3) ? 0 : gpu::filter_smem_fixed_bytes());
-        CK(cudaFuncSetAttribute(d->filter_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(d->filter_smem)));
+                         ((d->lean_single || im.filter_mode == 3)
+                              ? 0
+                              : (pair_queue_form() ? gpu::filter_smem_fixed_bytes() : gpu::filter2_smem_fixed_bytes()));
+        allow_max_smem(d->filter_fn, device);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
                                                          d->filter_smem));
         if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
     }
     CK(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device));
+    // A pageable cudaMemcpy may return before its DMA lands, and the scans run
+    // on non-blocking streams that do not wait for the legacy stream.
+    CK(cudaStreamSynchronize(cudaStreamLegacy));
     return d;
 }
 
@@ -352,11 +508,26 @@ struct Workspace {
     unsigned long long* h_small = nullptr; // pinned mirror
     uint4* d_flush = nullptr;
     size_t flush_n16 = 0;
+    // streamed hepfac_scan: D2H of each chunk's records on their own stream,
+    // a pinned staging ring for pageable callers, per-chunk count mirrors
+    cudaStream_t d2h = nullptr;
+    static constexpr int kStages = 3;
+    uint8_t* h_stage[kStages] = {};
+    size_t h_stage_cap = 0;
+    cudaEvent_t stage_done[kStages] = {};
+    cudaEvent_t cnt_done[2] = {};
+    unsigned long long* h_bases = nullptr; // pinned: [0, chunks] running record bases
+    size_t h_bases_cap = 0;
+    unsigned long long* h_flags = nullptr; // pinned: per slot, d_small[0..5] after its chunk
 
     explicit Workspace(int dev) : device(dev)
     {
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (auto& e : stage_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : cnt_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_flags), 2 * 8 * sizeof(unsigned long long), cudaHostAllocDefault));
         for (auto& e : ev) CK(cudaEventCreate(&e));
         for (int k = 0; k < 2; ++k) {
             CK(cudaEventCreateWithFlags(&h2d_done[k], cudaEventDisableTiming));
@@ -371,6 +542,13 @@ struct Workspace {
         cudaSetDevice(device);
         cudaStreamSynchronize(stream);
         cudaStreamSynchronize(copy);
+        cudaStreamSynchronize(d2h);
+        for (auto* p : h_stage) pinned_pool().release(p, h_stage_cap);
+        if (h_bases) pinned_pool().release(h_bases, h_bases_cap * sizeof(unsigned long long));
+        cudaFreeHost(h_flags);
+        for (auto& e : stage_done) cudaEventDestroy(e);
+        for (auto& e : cnt_done) cudaEventDestroy(e);
+        cudaStreamDestroy(d2h);
         for (void* p : {(void*)d_text, (void*)d_slot[0], (void*)d_slot[1], (void*)d_out, (void*)d_stage,
                         (void*)d_tile_count, (void*)d_tile_slot, (void*)d_chunk, (void*)d_bases, (void*)d_small,
                         (void*)d_flush, (void*)d_cand, (void*)d_cand_key, (void*)d_tile_ccount, (void*)d_tile_cslot,
@@ -433,7 +611,74 @@ struct Workspace {
     }
     // Clears the per-scan accumulators (overflow needs, error word).
     void begin_scan() { CK(cudaMemsetAsync(d_small, 0, 7 * sizeof(unsigned long long), stream)); }
+
+    void ensure_staging(size_t bytes)
+    {
+        if (bytes <= h_stage_cap) return;
+        CK(cudaStreamSynchronize(copy));
+        for (auto*& p : h_stage) {
+            pinned_pool().release(p, h_stage_cap);
+            p = nullptr;
+        }
+        size_t cap = 0;
+        for (auto*& p : h_stage) {
+            auto b = pinned_pool().acquire(bytes);
+            p = static_cast<uint8_t*>(b.first);
+            cap = b.second; // every block of one request has the same capacity
+        }
+        h_stage_cap = cap;
+    }
+    void ensure_host_bases(size_t n)
+    {
+        if (n <= h_bases_cap) return;
+        if (h_bases) pinned_pool().release(h_bases, h_bases_cap * sizeof(unsigned long long));
+        h_bases = nullptr;
+        auto b = pinned_pool().acquire(n * sizeof(unsigned long long));
+        h_bases = static_cast<unsigned long long*>(b.first);
+        h_bases_cap = b.second / sizeof(unsigned long long);
+    }
+
+    // Device bytes held by buffers that regrow on demand.
+    uint64_t held_bytes() const
+    {
+        return text_cap + 2 * slot_cap + out_cap * sizeof(hepfac_match_t) + stage_cap * sizeof(hepfac_match_t) +
+               cand_alloc * 2 + key_alloc * 4 + packed_cap * 4;
+    }
+    // Frees the large regrowable buffers (the next call re-allocates them).
+    void shed()
+    {
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaStreamSynchronize(copy));
+        CK(cudaStreamSynchronize(d2h));
+        auto drop = [](auto*& p, uint64_t& cap) {
+            cudaFree(p);
+            p = nullptr;
+            cap = 0;
+        };
+        drop(d_text, text_cap);
+        drop(d_out, out_cap);
+        drop(d_stage, stage_cap);
+        warp_cap = 0;
+        drop(d_cand, cand_alloc);
+        drop(d_cand_key, key_alloc);
+        cand_cap = 0;
+        drop(d_packed, packed_cap);
+        uint64_t c0 = slot_cap, c1 = slot_cap;
+        drop(d_slot[0], c0);
+        drop(d_slot[1], c1);
+        slot_cap = 0;
+    }
 };
+
+// A pooled workspace keeps at most this many device bytes of regrowable
+// buffers when its call returns (HEPFAC_POOL_KEEP_MIB, default 2048); a call
+// over a bigger text frees them instead of pinning them for the process.
+uint64_t pool_keep_bytes()
+{
+    uint64_t mib = 2048;
+    if (const char* s = std::getenv("HEPFAC_POOL_KEEP_MIB")) mib = std::strtoull(s, nullptr, 10);
+    return mib << 20;
+}
 
 std::mutex g_pool_mu;
 std::vector<std::vector<std::unique_ptr<Workspace>>> g_pool;
@@ -455,13 +700,29 @@ struct WorkspaceLease {
     ~WorkspaceLease()
     {
         if (!ws) return;
-        if (cudaStreamSynchronize(ws->stream) != cudaSuccess) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != ws->device) cudaSetDevice(ws->device);
+        struct Restore {
+            int d;
+            ~Restore()
+            {
+                if (d >= 0) cudaSetDevice(d);
+            }
+        } restore{prev};
+        if (cudaStreamSynchronize(ws->stream) != cudaSuccess || cudaStreamSynchronize(ws->d2h) != cudaSuccess) {
             cudaGetLastError();
             return; // poisoned: drop it
+        }
+        try {
+            if (ws->held_bytes() > pool_keep_bytes()) ws->shed();
+        } catch (...) {
+            return;
         }
         std::lock_guard<std::mutex> lk(g_pool_mu);
         g_pool[ws->device].push_back(std::move(ws));
     }
+    WorkspaceLease(WorkspaceLease&&) = default;
     Workspace* operator->() { return ws.get(); }
     Workspace& operator*() { return *ws; }
 };
@@ -657,89 +918,255 @@ uint64_t stream_chunk_bytes()
     return c;
 }
 
-// Streamed scan of host text: chunks of starts go H2D on the copy stream into
-// two device slots while the previous chunk's launch runs on the compute
-// stream; each launch places its records right after the previous chunk's
-// (device-side running base), so the output is ordered without host syncs
-// between chunks.  Chunk c's bytes carry the `halo` of right context its last
-// starts may read.
+// Host-to-host copy into a pinned staging buffer on several threads: one
+// memcpy thread moves ~10 GB/s, the PCIe Gen5 H2D it feeds ~55 GB/s.
+// HEPFAC_COPY_THREADS overrides the count (default: 3/4 of the host threads,
+// at most 12; on a 16-thread B200 host 8-12 threads reach ~43 GB/s, more do
+// not help).
+unsigned copy_threads()
+{
+    if (const char* s = std::getenv("HEPFAC_COPY_THREADS")) {
+        const long v = std::strtol(s, nullptr, 10);
+        if (v >= 1) return unsigned(std::min<long>(v, 64));
+    }
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return std::clamp(hw * 3 / 4, 1u, 12u);
+}
+
+// Persistent helper threads for par_memcpy (spawning threads per 64 MiB
+// chunk would cost ~10% of a streamed scan).  Concurrent callers share them.
+class CopyPool {
+public:
+    // Runs fn(0..parts-1): the caller runs part 0, helpers the rest (the
+    // pool grows to parts - 1 helpers on first need).
+    void run(unsigned parts, const std::function<void(unsigned)>& fn)
+    {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while (workers_.size() + 1 < parts) workers_.emplace_back([this] { loop(); });
+        }
+        struct Batch {
+            std::atomic<unsigned> left;
+            std::mutex mu;
+            std::condition_variable cv;
+        } batch;
+        batch.left = parts - 1;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (unsigned i = 1; i < parts; ++i)
+                tasks_.push_back([&batch, &fn, i] {
+                    fn(i);
+                    if (batch.left.fetch_sub(1) == 1) {
+                        std::lock_guard<std::mutex> g(batch.mu);
+                        batch.cv.notify_all();
+                    }
+                });
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lk(batch.mu);
+        batch.cv.wait(lk, [&] { return batch.left.load() == 0; });
+    }
+
+private:
+    void loop()
+    {
+        for (;;) {
+            std::function<void()> task;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !tasks_.empty(); });
+                task = std::move(tasks_.front());
+                tasks_.pop_front();
+            }
+            task();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> tasks_;
+    std::vector<std::thread> workers_;
+};
+
+void par_memcpy(void* dst, const void* src, size_t n)
+{
+    const size_t kSlice = size_t(4) << 20;
+    const unsigned T = unsigned(std::min<size_t>(copy_threads(), std::max<size_t>(1, n / kSlice)));
+    if (T <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    // helpers detach with the process (never joined: a static destructor
+    // must not wait on threads that a late caller may still be using)
+    static CopyPool* pool = new CopyPool;
+    pool->run(T, [&](unsigned i) {
+        const size_t lo = (n * i / T) & ~size_t(4095), hi = i + 1 == T ? n : (n * (i + 1) / T) & ~size_t(4095);
+        std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo);
+    });
+}
+
+// Pageable (not page-locked, not device) memory goes through the staging
+// ring; pinned host memory and device pointers are copied from directly.
+bool is_pageable(const void* p)
+{
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Streamed scan of host text.  Chunks of starts (with the `halo` of right
+// context their walks may read) go H2D on the copy stream into two device
+// slots while the previous chunk's launch runs on the compute stream; each
+// launch places its records right after the previous chunk's (device-side
+// running base), so the output is ordered without host syncs between chunks.
+// Pageable text is first copied (several host threads) into a ring of
+// kStages pinned buffers, so the DMA runs at pinned speed and the host copy
+// of chunk c+1 overlaps the DMA of chunk c.  With a `sink`, chunk c's records
+// go D2H (own stream) into the sink as soon as its kernel has finished,
+// overlapping chunks c+1...; without one they stay in ws.d_out.
 uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, uint64_t avail, uint64_t owned,
-                     uint64_t g0, uint64_t halo, ScanStats& st)
+                     uint64_t g0, uint64_t halo, MatchList* sink, ScanStats& st)
 {
     const uint64_t C = stream_chunk_bytes();
     const uint64_t n = (owned + C - 1) / C;
-    ws.ensure_slots(std::min(avail, C + halo));
+    const bool stage = is_pageable(text);
+    const uint64_t slot_bytes = std::min(avail, C + halo);
+    ws.ensure_slots(slot_bytes);
+    if (stage) ws.ensure_staging(slot_bytes);
     ws.regrow(ws.d_bases, ws.bases_cap, n + 1);
+    ws.ensure_host_bases(n + 1);
+    if (ws.out_cap < initial_records(owned)) ws.ensure_out(initial_records(owned));
+    st.staged = stage;
     for (int attempt = 0;; ++attempt) {
         ws.begin_scan();
         CK(cudaMemsetAsync(ws.d_bases, 0, sizeof(unsigned long long), ws.stream));
+        ws.h_bases[0] = 0;
+        if (sink) sink->size = 0;
         CK(cudaEventRecord(ws.ev[0], ws.stream));
         CK(cudaStreamWaitEvent(ws.copy, ws.ev[0], 0));
+        bool overflow = false;
+        // chunk k's base and overflow words are on the host once cnt_done fires
+        auto drain = [&](uint64_t k) {
+            const int slot = int(k & 1);
+            CK(cudaEventSynchronize(ws.cnt_done[slot]));
+            const unsigned long long* f = ws.h_flags + 8 * slot;
+            if (f[2] & 1u) fail(HEPFAC_ERR_INTERNAL, "terminal node spells no dictionary pattern");
+            const uint64_t b0 = ws.h_bases[k], b1 = ws.h_bases[k + 1];
+            if (overflow || f[0] || f[5] || b1 > ws.out_cap) {
+                overflow = true; // finish the pass, grow, re-run (fetch_small)
+                return;
+            }
+            if (!sink || b1 == b0) return;
+            if (b1 > sink->cap) { // extrapolate from the chunks so far
+                CK(cudaStreamSynchronize(ws.d2h));
+                sink->size = b0;
+                const double per = double(b1) / double(k + 1);
+                sink->reserve(std::max<uint64_t>(b1, uint64_t(per * double(n) * 1.125) + 1024));
+            }
+            CK(cudaMemcpyAsync(sink->data + b0, ws.d_out + b0, size_t(b1 - b0) * sizeof(hepfac_match_t),
+                               cudaMemcpyDeviceToHost, ws.d2h));
+            sink->size = b1;
+        };
         for (uint64_t c = 0; c < n; ++c) {
             const int slot = int(c & 1);
             const uint64_t lo = c * C, own = std::min(C, owned - lo), bytes = std::min(avail - lo, own + halo);
+            const uint8_t* src = text + lo;
+            if (stage) {
+                const int r = int(c % Workspace::kStages);
+                if (c >= uint64_t(Workspace::kStages)) CK(cudaEventSynchronize(ws.stage_done[r]));
+                par_memcpy(ws.h_stage[r], src, size_t(bytes));
+                src = ws.h_stage[r];
+            }
             if (c >= 2) CK(cudaStreamWaitEvent(ws.copy, ws.kern_done[slot], 0));
-            CK(cudaMemcpyAsync(ws.d_slot[slot], text + lo, size_t(bytes), cudaMemcpyHostToDevice, ws.copy));
+            CK(cudaMemcpyAsync(ws.d_slot[slot], src, size_t(bytes), cudaMemcpyDefault, ws.copy));
             CK(cudaEventRecord(ws.h2d_done[slot], ws.copy));
+            if (stage) CK(cudaEventRecord(ws.stage_done[c % Workspace::kStages], ws.copy));
             CK(cudaStreamWaitEvent(ws.stream, ws.h2d_done[slot], 0));
             if (c == 0) CK(cudaEventRecord(ws.ev[1], ws.stream));
             st.kernel_launches +=
                 enqueue_scan(dt, ws, ws.d_slot[slot], own, bytes, g0 + lo, ws.d_bases + c, ws.d_bases + c + 1);
             CK(cudaEventRecord(ws.kern_done[slot], ws.stream));
+            CK(cudaMemcpyAsync(ws.h_bases + c + 1, ws.d_bases + c + 1, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, ws.stream));
+            CK(cudaMemcpyAsync(ws.h_flags + 8 * slot, ws.d_small, 6 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, ws.stream));
+            CK(cudaEventRecord(ws.cnt_done[slot], ws.stream));
+            if (c >= 1) drain(c - 1);
         }
         CK(cudaEventRecord(ws.ev[2], ws.stream));
+        drain(n - 1);
         st.chunks = uint32_t(n);
-        if (fetch_small(ws, dt, C, ws.d_bases + n)) return records_of(ws);
+        if (!overflow) return ws.h_bases[n];
+        CK(cudaStreamSynchronize(ws.d2h));
+        if (fetch_small(ws, dt, C, ws.d_bases + n)) // cannot happen: some word said overflow
+            fail(HEPFAC_ERR_INTERNAL, "streamed scan overflow not confirmed by the device");
         st.relaunches++;
         if (attempt > 4) fail(HEPFAC_ERR_INTERNAL, "scan buffers keep overflowing");
     }
 }
 
-// Copies `text` in, scans, copies the sorted list out.  Texts up to two chunks
-// go to the device in one piece; longer ones are streamed chunk by chunk so
-// the H2D copy overlaps the kernels.
-std::unique_ptr<MatchList> scan_resident(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned,
-                                         uint64_t g0, int device = -1)
-{
-    auto out = std::make_unique<MatchList>();
+// One shard of starts on one device.  With a `sink` the records land in it
+// (overlapped D2H) and the workspace returns to the pool; without, `keep`
+// holds the workspace and its device-resident records for a later copy.
+struct ShardJob {
+    std::unique_ptr<WorkspaceLease> ws;
+    uint64_t total = 0;
     ScanStats st;
+};
+
+void run_shard(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned, uint64_t g0, int device,
+               MatchList* sink, ShardJob& job)
+{
+    ScanStats& st = job.st;
+    st = ScanStats{};
     st.bytes = owned;
-    if (owned == 0) {
-        t_stats = st;
-        return out;
-    }
+    if (owned == 0) return;
     const int dev = device >= 0 ? device : pick_device();
     st.device = dev;
     DeviceGuard g(dev);
     auto dt = t.device_image(dev);
-    if (dt->min_emit == UINT32_MAX || avail < dt->min_emit) {
-        t_stats = st;
-        return out;
-    }
-    WorkspaceLease ws(dev);
+    if (dt->min_emit == UINT32_MAX || avail < dt->min_emit) return;
+    job.ws = std::make_unique<WorkspaceLease>(dev);
+    Workspace& ws = **job.ws;
     uint64_t total;
-    const bool streamed = owned > 2 * stream_chunk_bytes() && dt->reach != UINT64_MAX;
-    if (streamed) {
-        total = stream_scan(*dt, *ws, text, avail, owned, g0, dt->reach ? dt->reach - 1 : 0, st);
-    } else {
-        ws->ensure_text(avail);
-        CK(cudaEventRecord(ws->ev[0], ws->stream));
-        CK(cudaMemcpyAsync(ws->d_text, text, size_t(avail), cudaMemcpyHostToDevice, ws->stream));
-        total = run_to_completion(*dt, *ws, owned, avail, g0, &st);
+    if (dt->reach != UINT64_MAX) {
+        total = stream_scan(*dt, ws, text, avail, owned, g0, dt->reach ? dt->reach - 1 : 0, sink, st);
+    } else { // cyclic loaded trie: walks have no bounded halo, so the text goes in one piece
+        ws.ensure_text(avail);
+        CK(cudaEventRecord(ws.ev[0], ws.stream));
+        CK(cudaMemcpyAsync(ws.d_text, text, size_t(avail), cudaMemcpyDefault, ws.stream));
+        total = run_to_completion(*dt, ws, owned, avail, g0, &st);
         st.chunks = 1;
+        if (sink) {
+            sink->allocate(size_t(total));
+            if (total)
+                CK(cudaMemcpyAsync(sink->data, ws.d_out, size_t(total) * sizeof(hepfac_match_t),
+                                   cudaMemcpyDeviceToHost, ws.d2h));
+        }
     }
-    out->allocate(size_t(total));
-    if (total)
-        CK(cudaMemcpyAsync(out->data, ws->d_out, size_t(total) * sizeof(hepfac_match_t), cudaMemcpyDeviceToHost,
-                           ws->stream));
-    CK(cudaEventRecord(ws->ev[3], ws->stream));
-    CK(cudaStreamSynchronize(ws->stream));
-    st.h2d_ms = elapsed_ms(ws->ev[0], ws->ev[1]);  // streamed: first chunk only
-    st.kernel_ms = elapsed_ms(ws->ev[1], ws->ev[2]); // streamed: kernels overlapped with later copies
-    st.d2h_ms = elapsed_ms(ws->ev[2], ws->ev[3]);
-    st.total_ms = elapsed_ms(ws->ev[0], ws->ev[3]);
+    job.total = total;
+    CK(cudaEventRecord(ws.ev[3], ws.d2h));
+    CK(cudaStreamSynchronize(ws.d2h));
+    CK(cudaStreamSynchronize(ws.stream));
+    st.h2d_ms = elapsed_ms(ws.ev[0], ws.ev[1]);  // streamed: first chunk only
+    st.kernel_ms = elapsed_ms(ws.ev[1], ws.ev[2]); // streamed: kernels overlapped with later copies
+    st.d2h_ms = std::max(0.0, elapsed_ms(ws.ev[2], ws.ev[3]));
+    st.total_ms = elapsed_ms(ws.ev[0], ws.ev[3]);
     st.matches = total;
-    t_stats = st;
+    if (sink) job.ws.reset(); // back to the pool
+}
+
+std::unique_ptr<MatchList> scan_one(const Trie& t, const uint8_t* text, uint64_t avail, uint64_t owned, uint64_t g0,
+                                    int device = -1)
+{
+    auto out = std::make_unique<MatchList>();
+    ShardJob job;
+    run_shard(t, text, avail, owned, g0, device, out.get(), job);
+    out->size = size_t(job.total);
+    t_stats = job.st;
     return out;
 }
 
@@ -775,57 +1202,68 @@ std::vector<int> scan_devices()
 
 // Multi-GPU hepfac_scan: contiguous shards of starts, each with
 // the halo its walks may read, scanned concurrently (one host thread per
-// shard); the shards' sorted lists concatenate in shard order, which is the
-// whole list's order -- the exclusive scan of per-shard counts is the host's
-// output offset of each shard.
+// shard) with their records left on their devices.  The exclusive scan of
+// the per-shard counts gives each shard's offset in the one host list, and
+// every device copies its sorted records straight to out + prefix[g]: shard
+// order is the whole list's order.
 std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t bytes)
 {
-    if (bytes == 0) return scan_resident(t, text, 0, 0, 0); // empty: never touches a device
+    if (bytes == 0) return scan_one(t, text, 0, 0, 0); // empty: never touches a device
     const std::vector<int> devs = scan_devices();
     constexpr uint64_t kMinShard = uint64_t(16) << 20;
     const uint64_t G = std::min<uint64_t>(devs.size(), std::max<uint64_t>(1, bytes / kMinShard));
-    if (G <= 1) return scan_resident(t, text, bytes, bytes, 0, devs[0]);
+    if (G <= 1) return scan_one(t, text, bytes, bytes, 0, devs[0]);
     const uint64_t reach = t.device_image(devs[0])->reach;
-    if (reach == UINT64_MAX) return scan_resident(t, text, bytes, bytes, 0, devs[0]); // cyclic: no halo bound
+    if (reach == UINT64_MAX) return scan_one(t, text, bytes, bytes, 0, devs[0]); // cyclic: no halo bound
     const uint64_t halo = reach ? reach - 1 : 0;
-    std::vector<std::unique_ptr<MatchList>> parts(G);
-    std::vector<ScanStats> stats(G);
+    std::vector<ShardJob> jobs(G);
     std::vector<std::exception_ptr> errs(G);
-    std::vector<std::thread> pool;
-    for (uint64_t g = 0; g < G; ++g)
-        pool.emplace_back([&, g] {
-            try {
-                const uint64_t lo = bytes * g / G, hi = bytes * (g + 1) / G;
-                const uint64_t avail = std::min(bytes - lo, hi - lo + halo);
-                parts[g] = scan_resident(t, text + lo, avail, hi - lo, lo, devs[g]);
-                stats[g] = t_stats;
-            } catch (...) {
-                errs[g] = std::current_exception();
-            }
-        });
-    for (auto& th : pool) th.join();
-    for (auto& e : errs)
-        if (e) std::rethrow_exception(e);
+    auto parallel = [&](auto&& fn) {
+        std::vector<std::thread> pool;
+        for (uint64_t g = 0; g < G; ++g)
+            pool.emplace_back([&, g] {
+                try {
+                    fn(g);
+                } catch (...) {
+                    errs[g] = std::current_exception();
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    };
+    parallel([&](uint64_t g) {
+        const uint64_t lo = bytes * g / G, hi = bytes * (g + 1) / G;
+        const uint64_t avail = std::min(bytes - lo, hi - lo + halo);
+        run_shard(t, text + lo, avail, hi - lo, lo, devs[g], nullptr, jobs[g]);
+    });
+    std::vector<uint64_t> prefix(G + 1, 0); // the count exchange: exclusive scan of shard totals
+    for (uint64_t g = 0; g < G; ++g) prefix[g + 1] = prefix[g] + jobs[g].total;
     auto out = std::make_unique<MatchList>();
-    uint64_t total = 0;
-    for (auto& p : parts) total += p->size;
-    out->allocate(size_t(total));
+    out->allocate(size_t(prefix[G]));
+    parallel([&](uint64_t g) {
+        if (!jobs[g].total) return;
+        Workspace& ws = **jobs[g].ws;
+        DeviceGuard dg(ws.device);
+        CK(cudaMemcpyAsync(out->data + prefix[g], ws.d_out, size_t(jobs[g].total) * sizeof(hepfac_match_t),
+                           cudaMemcpyDeviceToHost, ws.d2h));
+        CK(cudaStreamSynchronize(ws.d2h));
+    });
     ScanStats st;
     st.bytes = bytes;
     st.device = devs[0];
-    uint64_t at = 0;
     for (uint64_t g = 0; g < G; ++g) {
-        if (parts[g]->size) std::memcpy(out->data + at, parts[g]->data, parts[g]->size * sizeof(hepfac_match_t));
-        at += parts[g]->size;
-        st.kernel_launches += stats[g].kernel_launches;
-        st.chunks += stats[g].chunks;
-        st.relaunches += stats[g].relaunches;
-        st.h2d_ms = std::max(st.h2d_ms, stats[g].h2d_ms);
-        st.kernel_ms = std::max(st.kernel_ms, stats[g].kernel_ms);
-        st.d2h_ms = std::max(st.d2h_ms, stats[g].d2h_ms);
-        st.total_ms = std::max(st.total_ms, stats[g].total_ms);
+        const ScanStats& s = jobs[g].st;
+        st.kernel_launches += s.kernel_launches;
+        st.chunks += s.chunks;
+        st.relaunches += s.relaunches;
+        st.staged = st.staged || s.staged;
+        st.h2d_ms = std::max(st.h2d_ms, s.h2d_ms);
+        st.kernel_ms = std::max(st.kernel_ms, s.kernel_ms);
+        st.d2h_ms = std::max(st.d2h_ms, s.d2h_ms);
+        st.total_ms = std::max(st.total_ms, s.total_ms);
     }
-    st.matches = total;
+    st.matches = prefix[G];
     t_stats = st;
     return out;
 }
@@ -834,7 +1272,20 @@ std::unique_ptr<MatchList> gpu_scan_shard(const Trie& t, const uint8_t* text, ui
                                           uint64_t g0)
 {
     if (owned > avail) invalid("shard owns more starts than it has bytes");
-    return scan_resident(t, text, avail, owned, g0);
+    return scan_one(t, text, avail, owned, g0);
+}
+
+void trim_pools()
+{
+    std::vector<std::unique_ptr<Workspace>> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (auto& v : g_pool)
+            for (auto& w : v) drop.push_back(std::move(w));
+        g_pool.clear();
+    }
+    drop.clear(); // workspace destructors free device buffers and return pinned blocks
+    pinned_pool().trim(0);
 }
 
 uint64_t gpu_halo(const Trie& t)
@@ -882,18 +1333,23 @@ Throughput gpu_run_throughput(const Trie& t, const uint8_t* text, uint64_t bytes
     auto dt = t.device_image(dev);
     WorkspaceLease ws(dev);
     ws->ensure_text(bytes);
-    CK(cudaMemcpy(ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
-    if (dt->min_emit == UINT32_MAX || bytes < dt->min_emit) return r;
-    run_to_completion(*dt, *ws, bytes, bytes, 0, nullptr); // warm-up, untimed; sizes the buffers
+    CK(cudaMemcpyAsync(ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice, ws->stream));
+    CK(cudaStreamSynchronize(ws->stream));
+    // A trie that cannot match here launches nothing, but its runs are still
+    // timed (event pairs on the stream), so the report never carries seconds
+    // of 0 (the reference always times its runs, bench.cpp:64-76).
+    const bool can_match = dt->min_emit != UINT32_MAX && bytes >= dt->min_emit;
+    if (can_match) run_to_completion(*dt, *ws, bytes, bytes, 0, nullptr); // warm-up, untimed; sizes the buffers
     std::vector<hepfac_match_t> host;
     double sum_scan = 0, sum_merge = 0;
     for (uint32_t i = 0; i < runs; ++i) {
         ws->begin_scan();
         CK(cudaEventRecord(ws->ev[0], ws->stream));
-        enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0);
+        if (can_match) enqueue_scan(*dt, *ws, ws->d_text, bytes, bytes, 0);
         CK(cudaEventRecord(ws->ev[1], ws->stream));
-        if (!fetch_small(*ws, *dt, bytes)) fail(HEPFAC_ERR_INTERNAL, "scan buffers overflowed after warm-up");
-        r.matches = records_of(*ws);
+        if (can_match && !fetch_small(*ws, *dt, bytes))
+            fail(HEPFAC_ERR_INTERNAL, "scan buffers overflowed after warm-up");
+        r.matches = can_match ? records_of(*ws) : 0;
         host.resize(size_t(r.matches));
         CK(cudaEventRecord(ws->ev[2], ws->stream));
         if (r.matches)
@@ -916,7 +1372,7 @@ struct Session {
     std::shared_ptr<DeviceTrie> dt;
     std::unique_ptr<Workspace> ws;
     uint64_t bytes = 0, matches = 0, offset = 0, owned = 0;
-    bool complete = false, split = false;
+    bool complete = false, split = false, sized = false;
     uint32_t last_iterations = 0;
     std::vector<cudaEvent_t> evs;
     ~Session()
@@ -940,7 +1396,8 @@ Session* session_create(const Trie& t, const uint8_t* text, uint64_t bytes, uint
     s->offset = offset;
     s->owned = owned;
     s->ws->ensure_text(bytes);
-    CK(cudaMemcpy(s->ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(s->ws->d_text, text, size_t(bytes), cudaMemcpyHostToDevice, s->ws->stream));
+    CK(cudaStreamSynchronize(s->ws->stream));
     return s.release();
 }
 
@@ -961,6 +1418,10 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventCreate(&e));
         s->evs.push_back(e);
     }
+    // The first run sizes every buffer (candidates, staging, output) with
+    // untimed scans until one completes, so timed iterations never overflow.
+    if (can_match && !s->sized) run_to_completion(dt, ws, s->owned, s->bytes, s->offset, nullptr);
+    s->sized = true;
     ws.begin_scan();
     for (uint32_t i = 0; i < iterations; ++i) {
         if (flush_l2)
@@ -980,7 +1441,8 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
 void session_split(Session* s, uint32_t n, double* first_ms, double* second_ms, uint32_t* kernels_per_scan)
 {
     DeviceGuard g(s->ws->device);
-    if (kernels_per_scan) *kernels_per_scan = pipelined(*s->dt, s->owned) ? 2u : 1u;
+    if (kernels_per_scan)
+        *kernels_per_scan = pipelined(*s->dt, s->owned) ? (s->dt->sym_bits ? 3u : 2u) : 1u; // + pack pass
     n = std::min(n, s->last_iterations);
     for (uint32_t i = 0; i < n; ++i) {
         const double total = elapsed_ms(s->evs[3 * i], s->evs[3 * i + 2]);

@@ -12,13 +12,20 @@ namespace hfb {
 
 // Host-side result of a scan: the reference's vector<MatchResult>
 // (capi.cpp:31-33), held as a flat array of hepfac_match_t.
+// Lists of 1 MiB or more sit in pinned (page-locked) host memory from a
+// process-wide pool, so their D2H runs at PCIe speed; destroy returns the
+// block to the pool.
 struct MatchList {
     hepfac_match_t* data = nullptr;
     size_t size = 0;
+    size_t cap = 0;      // records the block holds
+    bool pinned = false;
     MatchList() = default;
     MatchList(const MatchList&) = delete;
     ~MatchList();
-    void allocate(size_t n);
+    void allocate(size_t n);  // size = n, contents undefined
+    void reserve(size_t n);   // capacity >= n, keeps the first `size` records
+    void release();
 };
 
 // Timing breakdown of the most recent hepfac_scan on this thread (device
@@ -28,6 +35,7 @@ struct ScanStats {
     uint64_t bytes = 0, matches = 0;
     uint32_t kernel_launches = 0, chunks = 0, relaunches = 0;
     int device = -1;
+    bool staged = false; // pageable text went through the pinned staging ring
 };
 
 // hepfac_scan: every occurrence, sorted by (start, length, id).
@@ -73,5 +81,9 @@ struct LayoutInfo {
 LayoutInfo layout_info(const Trie& t);
 
 int device_count();
+
+// Frees every pooled workspace (device buffers, streams) and pinned block
+// that no call is using (hepfac_b200_trim).
+void trim_pools();
 
 } // namespace hfb

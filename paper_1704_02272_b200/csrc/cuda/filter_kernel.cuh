@@ -257,7 +257,205 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
     if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
 }
 
+// ---- pair form, in-lane second level ---------------------------------------------
+//
+// Same tiles, loads, first level and candidate output as the queue form
+// above, with the second level done by each lane on its own first-level
+// survivors, reading their bytes back from the step staged contiguously in
+// shared memory (the step's 2 KiB + the 4 bytes after it).  The queue form
+// spends ~36% of its instructions building the queue and running full-warp
+// rounds on it; here a step costs max-over-lanes(survivors) iterations of a
+// ~20-instruction loop (about 6 at c3's 3.7% first-level pass rate), and the
+// final survivors (~0.1%) are placed in start order by one ballot per chunk.
+constexpr uint32_t kPStage = kFStep + 16;             // staged step + the word after it
+constexpr uint32_t kPWarpSmem = kPStage;
+
+__device__ __forceinline__ uint32_t f_pair_probe(const uint32_t* __restrict__ tab, uint32_t mid, uint32_t shift)
+{
+    return tab[(mid * kPairMul) >> shift];
+}
+
+__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const __grid_constant__ FilterArgs a)
+{
+    extern __shared__ __align__(128) uint8_t fsmem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
+    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
+    __syncthreads();
+    uint8_t* stage = fsmem + size_t(a.table_words) * 4 + warp * kPWarpSmem;
+    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+    const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+
+    const uint32_t gw = blockIdx.x * kFWarps + warp, W = gridDim.x * kFWarps;
+    const uint32_t shift = a.pair_shift;
+    const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
+    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
+    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
+    const uint32_t cap = uint32_t(min(a.cand_cap, uint64_t(0xFFFFFFFFu)));
+    uint32_t cursor = 0;
+    const uint32_t below = (1u << lane) - 1u;
+    const uint32_t my = stage_s + 16u * lane; // this lane's 16 bytes of chunk 0
+
+    auto load = [&](uint64_t at) -> uint4 {
+        const uint64_t p = at + 16u * lane;
+        return p < avail16 ? __ldg(reinterpret_cast<const uint4*>(a.text + p)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    // bytes [so, so + 4) of the staged step
+    auto staged4 = [&](uint32_t so) -> uint32_t {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + (so >> 2);
+        uint32_t t;
+        asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(t) : "r"(w[0]), "r"(w[1]), "r"(so));
+        return t;
+    };
+
+    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
+        const uint64_t lo = tile * kFTile;
+        const uint32_t slot = cursor;
+        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
+        const uint32_t steps = (rem + kFStep - 1) / kFStep;
+        uint4 nxt[kFChunks];
+        if (steps) {
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(lo + b * kFChunk);
+        }
+        for (uint32_t s = 0; s < steps; ++s) {
+            const uint64_t sbase = lo + uint64_t(s) * kFStep;
+            uint4 cur[kFChunks];
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
+            if (s + 1 < steps) {
+                const uint64_t nb = sbase + kFStep;
+                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
+                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
+#pragma unroll
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
+                } else {
+#pragma unroll
+                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
+                }
+            }
+            // the word after the step (lane 0 of the next step's first chunk)
+            uint32_t tail = 0;
+            if (lane == 31 && sbase + kFStep < avail16)
+                tail = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
+            __syncwarp(); // the previous step's staged bytes are no longer read
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b)
+                *reinterpret_cast<uint4*>(stage + b * kFChunk + 16u * lane) = cur[b];
+            if (lane == 31) *reinterpret_cast<uint32_t*>(stage + kFStep) = tail;
+            __syncwarp();
+
+            const bool full = (s + 1) * kFStep <= rem; // warp-uniform: every start of the step may report
+            uint32_t m01 = 0, m23 = 0; // first-level survivors, 16 bits per chunk
+#pragma unroll
+            for (uint32_t b = 0; b < kFChunks; ++b) {
+                uint32_t ov; // the 4 bytes after this lane's 16
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ov) : "r"(my + b * kFChunk + 16u));
+                const uint32_t w[5] = {cur[b].x, cur[b].y, cur[b].z, cur[b].w, ov};
+                uint32_t m = f_pair_level1(w, tbase, shift);
+                if (!full) {
+                    const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
+                    m &= r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+                }
+                if (b == 0) m01 = m;
+                else if (b == 1) m01 |= m << 16;
+                else if (b == 2) m23 = m;
+                else m23 |= m << 16;
+            }
+            if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
+
+            // second level, in-lane: the other role of each first-level
+            // survivor, highest bit first (x: chunks 0-1, y: chunks 2-3; bit j
+            // = chunk j/16, position j%16 of the lane's slice).  One loop over
+            // both words: a step costs max over lanes of the lane's survivors.
+            // Failing bits are cleared from m01 / m23.
+            {
+                uint32_t x = m01, y = m23;
+                const uint32_t base = 16u * lane;
+                while (x | y) {
+                    const bool first = x != 0;
+                    const uint32_t j = 31u - __clz(first ? x : y);
+                    const uint32_t bit = 1u << j;
+                    if (first) x ^= bit;
+                    else y ^= bit;
+                    // staging offset: chunk * 512 + 16 * lane + position
+                    const uint32_t so = (first ? base : base + 2u * kFChunk) + j + (j >> 4) * (kFChunk - 16u);
+                    const uint32_t t = staged4(so);             // bytes p0 p1 p2 p3 of the start
+                    const bool odd = j & 1u;                    // odd starts passed role B: test A
+                    const uint32_t mid = odd ? (t >> 8) : t;    // A: H(p1 p2 p3); B: H(p0 p1 p2)
+                    const uint32_t amt = odd ? t : (t >> 24);   // A: bit p0;       B: bit p3
+                    const uint32_t word = s_tab[(mid * kPairMul) >> shift];
+                    if (int32_t(word << (amt & 31u)) >= 0) {
+                        if (first) m01 ^= bit;
+                        else m23 ^= bit;
+                    }
+                }
+            }
+            if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
+            // final survivors in start order (chunk, lane, position): one warp
+            // scan of the lane's four per-chunk counts packed in 8-bit fields
+            // (exact while every lane has at most 7 survivors in the step)
+            const uint32_t n01 = __popc(m01), n23 = __popc(m23);
+            const uint32_t cnt = (__popc(m01 & 0xFFFFu)) | ((n01 - __popc(m01 & 0xFFFFu)) << 8) |
+                                 (__popc(m23 & 0xFFFFu) << 16) | ((n23 - __popc(m23 & 0xFFFFu)) << 24);
+            if (__any_sync(0xFFFFFFFFu, n01 + n23 > 7u)) {
+                // dense step: chunk by chunk, one scan each
+#pragma unroll
+                for (uint32_t b = 0; b < kFChunks; ++b) {
+                    const uint32_t f = ((b < 2 ? m01 : m23) >> (16u * (b & 1u))) & 0xFFFFu;
+                    const uint32_t n = __popc(f);
+                    uint32_t incl = n;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                        if (lane >= uint32_t(d)) incl += u;
+                    }
+                    uint32_t at = cursor + incl - n;
+                    for (uint32_t m = f; m; m &= m - 1, ++at) {
+                        const uint32_t so = b * kFChunk + 16u * lane + uint32_t(__ffs(m) - 1);
+                        if (at < cap) {
+                            region[at] = uint16_t(s * kFStep + so);
+                            keys[at] = staged4(so);
+                        }
+                    }
+                    cursor += __shfl_sync(0xFFFFFFFFu, incl, 31);
+                }
+                continue;
+            }
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= uint32_t(d)) incl += u;
+            }
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            // byte b: survivors before this lane's chunk-b ones (earlier chunks + earlier lanes)
+            const uint32_t pos = incl - cnt + tot * 0x01010100u;
+            if (m01 | m23) {
+#pragma unroll
+                for (uint32_t b = 0; b < kFChunks; ++b) {
+                    uint32_t at = cursor + ((pos >> (8u * b)) & 0xFFu);
+                    for (uint32_t m = ((b < 2 ? m01 : m23) >> (16u * (b & 1u))) & 0xFFFFu; m; m &= m - 1, ++at) {
+                        const uint32_t so = b * kFChunk + 16u * lane + uint32_t(__ffs(m) - 1);
+                        if (at < cap) {
+                            region[at] = uint16_t(s * kFStep + so);
+                            keys[at] = staged4(so);
+                        }
+                    }
+                }
+            }
+            cursor += (tot * 0x01010101u) >> 24;
+        }
+        if (lane == 0) {
+            a.tile_ccount[tile] = cursor - slot;
+            a.tile_cslot[tile] = uint32_t(slot);
+        }
+    }
+    if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+}
+
 constexpr uint32_t filter_smem_fixed_bytes() { return kFWarps * kFWarpSmem; }
+constexpr uint32_t filter2_smem_fixed_bytes() { return kFWarps * kPWarpSmem; }
 
 // ---- single-probe form -------------------------------------------------------
 

@@ -83,7 +83,7 @@ class _ScanStats(C.Structure):
     _fields_ = [("h2d_ms", C.c_double), ("kernel_ms", C.c_double), ("d2h_ms", C.c_double),
                 ("total_ms", C.c_double), ("bytes", C.c_uint64), ("matches", C.c_uint64),
                 ("kernel_launches", C.c_uint32), ("chunks", C.c_uint32), ("relaunches", C.c_uint32),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("staged", C.c_uint32)]
 
 
 class _LayoutInfo(C.Structure):
@@ -167,6 +167,7 @@ _B200_PROTOTYPES = [
     ("hepfac_b200_session_fetch", C.c_int, [_P, _PP]),
     ("hepfac_b200_session_destroy", None, [_P]),
     ("hepfac_b200_layout_info", C.c_int, [_P, C.POINTER(_LayoutInfo)]),
+    ("hepfac_b200_trim", C.c_int, []),
 ]
 
 ABI_SYMBOLS = [p[0] for p in _PROTOTYPES]
@@ -324,6 +325,10 @@ class Library:
         s = _ScanStats()
         self.check(self.dll.hepfac_b200_last_scan_stats(C.byref(s)))
         return {f: getattr(s, f) for f, _ in _ScanStats._fields_}
+
+    def trim(self) -> None:
+        """hepfac_b200_trim: free pooled workspaces and pinned blocks."""
+        self.check(self.dll.hepfac_b200_trim())
 
     def layout_info(self, trie: "Trie") -> dict:
         s = _LayoutInfo()

@@ -7,7 +7,9 @@ sweeps (config 4) use the library's own hepfac_patterns_generate with the
 reference's derive_seed (bench.cpp:14-24).  Texts >= 1 GiB come from a
 counter-based generator (numpy PCG64) because the reference's MT19937 corpus
 generator runs at ~200 MB/s; the same buffer feeds every arm.  Plants: one
-pattern occurrence per 4 KiB, round robin over the set.
+pattern occurrence per 4 KiB, round robin over the set.  The text is built
+from independent 16 MiB blocks, so any global range (a rank's shard plus its
+halo) can be generated on its own.
 """
 from __future__ import annotations
 
@@ -106,6 +108,32 @@ def plant(text: np.ndarray, patterns: List[bytes], every: int = 4096, seed: int 
     return n
 
 
+# The synthetic text of a workload is one global byte string made of
+# independent 16 MiB blocks: block i is random_text(seed, i) with its own
+# planted occurrences.  Any range of it can be generated on its own, so every
+# rank of a sharded run builds exactly its global bytes [lo, hi) -- halo
+# included -- and a one-rank scan of the same global text is the check.
+BLOCK = 16 * MiB
+
+
+def _block(seed: int, symbols: bytes, patterns, i: int) -> np.ndarray:
+    b = random_text(seed * 7919 + 1_000_003 * i, symbols, BLOCK)
+    if patterns:
+        plant(b, patterns, 4096, seed + 31 * i, base=i * (BLOCK // 4096))
+    return b
+
+
+def text_range(seed: int, symbols: bytes, patterns, lo: int, hi: int) -> np.ndarray:
+    out = np.empty(max(0, hi - lo), dtype=np.uint8)
+    at = lo
+    while at < hi:
+        i, off = divmod(at, BLOCK)
+        n = min(BLOCK - off, hi - at)
+        out[at - lo:at - lo + n] = _block(seed, symbols, patterns, i)[off:off + n]
+        at += n
+    return out
+
+
 @dataclass
 class Workload:
     name: str
@@ -117,12 +145,14 @@ class Workload:
     gen_count: int = 0  # fixed-length sets generated by the library itself
     gen_length: int = 0
 
-    def make_text(self, nbytes: Optional[int] = None, offset_seed: int = 0) -> np.ndarray:
+    def make_text(self, nbytes: Optional[int] = None, lo: int = 0) -> np.ndarray:
+        """Bytes [lo, lo + nbytes) of the workload's global text."""
         n = self.text_bytes if nbytes is None else nbytes
-        t = random_text(self.seed * 7919 + offset_seed, self.symbols, n)
-        if self.patterns:
-            plant(t, self.patterns, 4096, self.seed + offset_seed)
-        return t
+        if self.patterns is None:
+            # config 4's fixed-length set comes from the library's generator:
+            # without it no occurrence could be planted
+            raise ValueError(f"{self.name}: call build_trie(lib, workload) before make_text (plants the set)")
+        return text_range(self.seed, self.symbols, self.patterns, lo, lo + n)
 
 
 def config(name: str, text_bytes: Optional[int] = None, sigma: int = 256, count: int = 0) -> Workload:

@@ -38,6 +38,7 @@ def main():
         t0 = time.perf_counter()
         w = workloads.config(name, **kw)
         nbytes = args.bytes if name != "c1" else 16 << 20
+        workloads.build_trie(lib, w, "full")  # c4: the library generates the set; make_text plants it
         text = w.make_text(nbytes)
         gen_s = time.perf_counter() - t0
         for state in args.states.split(","):
