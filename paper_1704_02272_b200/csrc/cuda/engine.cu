@@ -1288,11 +1288,15 @@ void trim_pools()
     pinned_pool().trim(0);
 }
 
+// The halo is a property of the trie (its longest walk), computed by the
+// host-side image builder, so shard planning works on hosts without a GPU
+// (e.g. a coordinator, or the CPU tests of the multi-process path).
 uint64_t gpu_halo(const Trie& t)
 {
-    const int dev = pick_device();
-    auto dt = t.device_image(dev);
-    return dt->reach == UINT64_MAX ? UINT64_MAX : (dt->reach ? dt->reach - 1 : 0);
+    uint64_t reach;
+    if (device_count() > 0) reach = t.device_image(pick_device())->reach;
+    else reach = build_gpu_image(t, image_options_from_env()).reach;
+    return reach == UINT64_MAX ? UINT64_MAX : (reach ? reach - 1 : 0);
 }
 
 LayoutInfo layout_info(const Trie& t)

@@ -19,6 +19,11 @@ from typing import Callable, Optional
 import numpy as np
 
 
+# hepfac_b200_halo reports an unbounded halo (a cyclic loaded trie) as
+# UINT64_MAX; Library.halo maps it to None.
+UNBOUNDED = (1 << 64) - 1
+
+
 @dataclass(frozen=True)
 class Shard:
     rank: int
@@ -32,11 +37,11 @@ class Shard:
         return self.end - self.lo
 
 
-def plan(n: int, world: int, rank: int, halo: int) -> Shard:
+def plan(n: int, world: int, rank: int, halo: Optional[int]) -> Shard:
     """Contiguous shard of an n-byte text for `rank` of `world`."""
     if not (0 <= rank < world):
         raise ValueError("rank out of range")
-    if halo < 0:
+    if halo is None or halo < 0 or halo >= UNBOUNDED:
         raise ValueError("unbounded walks (cyclic trie): shards cannot be used")
     lo = rank * n // world
     hi = (rank + 1) * n // world

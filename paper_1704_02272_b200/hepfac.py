@@ -310,10 +310,12 @@ class Library:
     def device_count(self) -> int:
         return self.dll.hepfac_b200_device_count()
 
-    def halo(self, trie: "Trie") -> int:
+    def halo(self, trie: "Trie") -> Optional[int]:
+        """Bytes of right context a shard needs; None when unbounded (a cyclic
+        loaded trie: hepfac_b200_halo reports UINT64_MAX)."""
         v = C.c_uint64()
         self.check(self.dll.hepfac_b200_halo(trie.h, C.byref(v)))
-        return v.value
+        return None if v.value == (1 << 64) - 1 else v.value
 
     def scan_shard(self, trie: "Trie", text, offset: int, owned: int) -> np.ndarray:
         arr = _as_u8(text)

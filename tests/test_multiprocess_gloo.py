@@ -1,9 +1,12 @@
 """The N>1 path on CPU: world_size 2 (and 3) over gloo.  Each rank plans its
 shard, scans it, and takes its global offset from the all_gather count
-exchange (paper_1704_02272_b200/dist.py).  The per-rank scanner here is the C
-oracle restricted to the shard's starts -- the host-side plumbing (shard and
-halo arithmetic, count exchange, ordering) is what is under test; the GPU
-scan_shard itself is checked against whole-text scans in test_gpu_parity.py."""
+exchange (paper_1704_02272_b200/dist.py).  Without a GPU the per-rank scanner
+is the C oracle or the compiled reference restricted to the shard's starts;
+the shard and halo arithmetic (the halo from the product library), the global
+block text, the count exchange and the ordering are what is under test.  The
+GPU scan_shard itself is checked against whole-text scans in
+test_gpu_parity.py, and bench.py --check compares the rank-order
+concatenation with a one-rank scan on the GPU box."""
 import os
 import socket
 
@@ -85,6 +88,69 @@ def test_sharded_scan_equals_whole_text(world):
     assert np.array_equal(got, want)
 
 
+def _workload_worker(rank, world, port, q, per_rank):
+    # One global text (workloads: 16 MiB blocks, any range reproducible),
+    # each rank generating only its own bytes [lo, end) -- halo included --
+    # the halo taken from the product library (hepfac_b200_halo works without
+    # a GPU), shards scanned by the compiled reference through the same C ABI
+    # and restricted to the rank's starts, offsets from the count exchange.
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1704_02272_b200 import hepfac, workloads
+        ref = oracle.ref_library()
+        lib = hepfac.lib()
+        w = workloads.config("c1")
+        t, _ = workloads.build_trie(lib, w, "s1trunc")
+        halo = lib.halo(t)
+        rt, _ = workloads.build_trie(ref, w, "s1trunc")
+        shard = D.plan(per_rank * world, world, rank, halo)
+        mine = w.make_text(shard.nbytes, lo=shard.lo)
+
+        def scanner(b, lo, owned):
+            recs = ref.scan(rt, b, workers=2)
+            recs = recs[recs["start"] < owned].copy()
+            recs["start"] += lo
+            return recs
+
+        recs, off, total = D.scan_sharded(mine, shard, scanner)
+        allrecs = D.gather_all(recs)
+        q.put((rank, off, total, halo, allrecs.tobytes() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_workload_text_with_product_halo():
+    import oracle
+    ref = oracle.ref_library()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    from paper_1704_02272_b200 import hepfac, workloads
+    world, per_rank = 3, (11 << 20) + 7  # shard seams inside and across 16 MiB blocks
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_workload_worker, args=(r, world, port, q, per_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = workloads.config("c1")
+    rt, _ = workloads.build_trie(ref, w, "s1trunc")
+    whole = w.make_text(per_rank * world)
+    want = ref.scan(rt, whole, workers=4)
+    assert results[0][3] == 31  # longest c1 pattern (32) - 1
+    assert {r[2] for r in results} == {want.size}
+    assert [r[1] for r in results] == sorted(r[1] for r in results)
+    got = np.frombuffer(results[0][4], dtype=want.dtype)
+    assert got.tobytes() == want.tobytes() and want.size > 5000
+
+
 def test_plan_covers_every_start_once():
     for n in (0, 1, 7, 4096, 100003):
         for world in (1, 2, 3, 8):
@@ -95,6 +161,10 @@ def test_plan_covers_every_start_once():
             assert all(s.end == min(n, s.lo + s.owned + 31) for s in shards)
     with pytest.raises(ValueError):
         D.plan(10, 2, 0, -1)
+    with pytest.raises(ValueError):  # a cyclic trie's unbounded halo
+        D.plan(10, 2, 0, D.UNBOUNDED)
+    with pytest.raises(ValueError):
+        D.plan(10, 2, 0, None)
 
 
 def test_reference_arm_under_torchrun():
