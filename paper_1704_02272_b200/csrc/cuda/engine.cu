@@ -259,7 +259,6 @@ struct DeviceTrie {
     bool grouped = false, identity = false;
     int kw = 0;
     bool pair = false;          // two-pass pipeline: filter pass + candidate-walking pass
-    bool lean_single = false;   // its filter pass is the single-probe form
     void (*filter_fn)(gpu::FilterArgs) = nullptr;
     double filter_pass = 1.0;
     KernelFn kernel = nullptr;
@@ -406,7 +405,6 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.jump_ext = im.jump_ext.empty() ? nullptr : d->upload(im.jump_ext);
     v.min_emit = im.min_emit;
 
-    d->lean_single = im.filter_mode == 1 && im.lean_single;
     // one-pass (fused) kernel: always available
     d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
     d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
@@ -415,7 +413,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     // two-pass pipeline (always for symbol keys: the one-pass kernel reads byte keys)
     d->sym_bits = im.sym_bits;
-    d->pair = ((im.filter_mode == 2 || d->lean_single) && pair_pipeline_enabled()) || im.filter_mode == 3;
+    d->pair = (im.filter_mode == 2 && pair_pipeline_enabled()) || im.filter_mode == 3;
     if (d->pair) {
         d->pipeline_min = im.filter_mode == 3 ? 0 : pipeline_min_bytes();
         if (im.filter_mode == 3) {
@@ -426,10 +424,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                                           : (im.sym_bits == 2 ? gpu::pfac_pack_symbols_kernel<2>
                                                               : gpu::pfac_pack_symbols_kernel<4>);
         } else {
-            d->filter_fn = !d->lean_single ? (pair_queue_form() ? gpu::pfac_pair_filter_kernel
-                                                                : gpu::pfac_pair_filter2_kernel)
-                                           : (d->kw == 3 ? gpu::pfac_single_filter_kernel<3>
-                                                         : gpu::pfac_single_filter_kernel<2>);
+            d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_kernel : gpu::pfac_pair_filter2_kernel;
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
@@ -438,7 +433,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                                                          int(gpu::kCWarps * 32), d->walk_smem));
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         d->filter_smem = size_t(v.filter_words) * 4 +
-                         ((d->lean_single || im.filter_mode == 3)
+                         (im.filter_mode == 3
                               ? 0
                               : (pair_queue_form() ? gpu::filter_smem_fixed_bytes() : gpu::filter2_smem_fixed_bytes()));
         allow_max_smem(d->filter_fn, device);
@@ -796,7 +791,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         const uint64_t fwarps = fgrid * gpu::kFWarps;
         ws.ensure_ctiles(l.n_ftiles);
         // expected: <= ~1% of starts survive; regions grow on overflow
-        if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / (dt.lean_single ? 64 : 256) / fwarps + 256);
+        if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / 256 / fwarps + 256);
         ws.ensure_cand(fwarps, ws.cand_cap);
         gpu::FilterArgs f{};
         f.table = dt.view.filter;
@@ -1319,7 +1314,7 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
-    li.filter_mode = d->kw == 0 ? 0u : (d->sym_bits ? 3u : ((d->pair && !d->lean_single) ? 2u : 1u));
+    li.filter_mode = d->kw == 0 ? 0u : (d->sym_bits ? 3u : (d->pair ? 2u : 1u));
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }

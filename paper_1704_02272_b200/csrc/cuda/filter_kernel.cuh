@@ -58,8 +58,7 @@ struct FilterArgs {
     uint32_t* tile_ccount;
     uint32_t* tile_cslot;
     unsigned long long* cand_need; // max entries any warp needed (overflow sizing)
-    // single-probe form (pfac_single_filter_kernel): k-byte key, table of
-    // table_words words (layout.hpp); symbol form: k symbols
+    // symbol form: k symbols per key
     uint32_t filter_k;
     const uint32_t* packed;  // symbol form: the text packed by pfac_pack_symbols_kernel
 };
@@ -456,156 +455,6 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const _
 
 constexpr uint32_t filter_smem_fixed_bytes() { return kFWarps * kFWarpSmem; }
 constexpr uint32_t filter2_smem_fixed_bytes() { return kFWarps * kPWarpSmem; }
-
-// ---- single-probe form -------------------------------------------------------
-
-// Bit j = start j of the 16-start slice passes the single-probe filter.
-// w[0..5] = the slice's 16 bytes and the next 8.  KW: 2 = k in 5..8, 3 = k == 4.
-template <int KW>
-__device__ __forceinline__ uint32_t f_single_level1(const uint32_t (&w)[6], uint32_t tbase, uint32_t mask4, uint32_t mhi)
-{
-    uint32_t m0 = 0, m1 = 0; // two independent chains, MSB-first
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const uint32_t lo = (j & 3) ? __funnelshift_r(w[j >> 2], w[(j >> 2) + 1], 8 * (j & 3)) : w[j >> 2];
-        uint32_t key = lo;
-        if (KW == 2) {
-            const uint32_t hi =
-                ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
-            key = lo + hi * 0x85EBCA77u; // filter_fold
-        }
-        const uint32_t word = f_lds(tbase + (__umulhi(key, kFilterMul) & mask4)); // filter_word(key) * 4
-        uint32_t& m = j < 8 ? m0 : m1;
-        m = __funnelshift_l(__funnelshift_l(0u, word, key), m, 1);
-    }
-    return __brev((m0 << 24) | (m1 << 16));
-}
-
-// Lean first pass for single-probe tries whose filter passes few starts
-// (<= ~2.5%): the same tiling, loads and candidate output as the pair form,
-// one shared-memory probe per start, survivors written directly (the walking
-// pass re-checks their 4-byte prefix).
-template <int KW>
-__global__ void __launch_bounds__(kFThreads, 1) pfac_single_filter_kernel(const __grid_constant__ FilterArgs a)
-{
-    extern __shared__ __align__(128) uint8_t fsmem[];
-    const uint32_t tid = threadIdx.x, lane = tid & 31u;
-    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
-    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
-    __syncthreads();
-    const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
-    const uint32_t mask4 = (a.table_words - 1u) << 2;
-    const uint32_t k = a.filter_k;
-    const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
-
-    const uint32_t gw = blockIdx.x * kFWarps + (tid >> 5), W = gridDim.x * kFWarps;
-    const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
-    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
-    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
-    uint64_t cursor = 0;
-    const uint32_t below = (1u << lane) - 1u;
-    auto load = [&](uint64_t at) -> uint4 {
-        const uint64_t p = at + 16u * lane;
-        return p < avail16 ? __ldg(reinterpret_cast<const uint4*>(a.text + p)) : make_uint4(0u, 0u, 0u, 0u);
-    };
-
-    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
-        const uint64_t lo = tile * kFTile;
-        const uint64_t slot = cursor;
-        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
-        const uint32_t steps = (rem + kFStep - 1) / kFStep;
-        uint4 nxt[kFChunks];
-        if (steps) {
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(lo + b * kFChunk);
-        }
-        for (uint32_t s = 0; s < steps; ++s) {
-            const uint64_t sbase = lo + uint64_t(s) * kFStep;
-            uint4 cur[kFChunks];
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
-            if (s + 1 < steps) {
-                const uint64_t nb = sbase + kFStep;
-                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
-                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
-#pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
-                } else {
-#pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
-                }
-            }
-            uint2 tail = make_uint2(0u, 0u); // lane 31's overhang of the last chunk
-            if (lane == 31 && sbase + kFStep < avail16)
-                tail = __ldg(reinterpret_cast<const uint2*>(a.text + sbase + kFStep));
-            const bool full = (s + 1) * kFStep <= rem;
-            uint32_t keep[kFChunks];
-            uint32_t many = 0;
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) {
-                const bool last = b + 1 == kFChunks;
-                const uint32_t sx = (lane == 0 && !last) ? cur[(b + 1) % kFChunks].x : cur[b].x;
-                const uint32_t sy = (lane == 0 && !last) ? cur[(b + 1) % kFChunks].y : cur[b].y;
-                uint32_t ox = __shfl_sync(0xFFFFFFFFu, sx, (lane + 1) & 31u);
-                uint32_t oy = __shfl_sync(0xFFFFFFFFu, sy, (lane + 1) & 31u);
-                if (lane == 31 && last) ox = tail.x, oy = tail.y;
-                const uint32_t w[6] = {cur[b].x, cur[b].y, cur[b].z, cur[b].w, ox, oy};
-                uint32_t m = f_single_level1<KW>(w, tbase, mask4, mhi);
-                if (!full) {
-                    const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
-                    m &= r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
-                }
-                keep[b] = m;
-                many |= m & (m - 1);
-            }
-            if (!__any_sync(0xFFFFFFFFu, keep[0] | keep[1] | keep[2] | keep[3])) continue;
-            auto text4 = [&](uint64_t pos) -> uint32_t { // a survivor's first 4 bytes (L1/L2 hits)
-                const uint32_t* p = reinterpret_cast<const uint32_t*>(a.text + (pos & ~3ull));
-                return __funnelshift_r(__ldg(p), __ldg(p + 1), 8u * uint32_t(pos & 3u));
-            };
-            const bool general = __any_sync(0xFFFFFFFFu, many != 0);
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) {
-                const uint32_t first = s * kFStep + b * kFChunk + 16u * lane; // tile offset
-                if (!general) { // at most one survivor per lane: a ballot places it
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep[b] != 0);
-                    if (keep[b]) {
-                        const uint64_t at = cursor + __popc(bal & below);
-                        const uint32_t j = __ffs(keep[b]) - 1;
-                        if (at < a.cand_cap) {
-                            region[at] = uint16_t(first + j);
-                            keys[at] = text4(lo + first + j);
-                        }
-                    }
-                    cursor += __popc(bal);
-                } else { // a warp scan of the per-lane counts
-                    const uint32_t n = __popc(keep[b]);
-                    uint32_t incl = n;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-                        if (lane >= uint32_t(d)) incl += u;
-                    }
-                    uint64_t at = cursor + incl - n;
-                    for (uint32_t m = keep[b]; m; m &= m - 1, ++at) {
-                        const uint32_t j = __ffs(m) - 1;
-                        if (at < a.cand_cap) {
-                            region[at] = uint16_t(first + j);
-                            keys[at] = text4(lo + first + j);
-                        }
-                    }
-                    cursor += __shfl_sync(0xFFFFFFFFu, incl, 31);
-                }
-            }
-        }
-        if (lane == 0) {
-            a.tile_ccount[tile] = uint32_t(cursor - slot);
-            a.tile_cslot[tile] = uint32_t(slot);
-        }
-    }
-    if (lane == 0 && cursor > a.cand_cap) atomicMax(a.cand_need, (unsigned long long)cursor);
-}
-
 
 // ---- symbol-key form (small alphabets) ------------------------------------------
 

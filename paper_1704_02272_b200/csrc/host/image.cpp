@@ -46,7 +46,6 @@ ImageOptions image_options_from_env()
     }
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_JUMP_EXT")) o.jump_ext = std::strtol(s, nullptr, 10) != 0;
-    if (const char* s = std::getenv("HEPFAC_LEAN_SINGLE")) o.lean_single = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
         const std::string m = s;
@@ -586,12 +585,11 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             if (opt.filter_mode == 1) use_pair = false;
             if (opt.filter_mode == 2) use_pair = k >= 4;
             // Two-pass pipeline (lean filter pass, then the walking pass) for
-            // the pair form and for a selective single probe (k >= 4): the
-            // walking pass re-checks survivors' first 4 bytes in shared memory.
-            // Measured (c4 sigma=20, k=7): 1.22 TB/s against 1.26 for the fused
-            // kernel, so it is opt-in (HEPFAC_LEAN_SINGLE=1).
-            const bool lean_single = opt.lean_single && !use_pair && k >= 4 && p_single <= 0.025;
-            if (use_pair || lean_single) {
+            // the pair form: the walking pass re-checks survivors' first 4
+            // bytes in shared memory.  (A single-probe filter pass was measured
+            // slower than the fused kernel, c4 sigma=20: 1.22 against 1.26 TB/s,
+            // and was removed.)
+            if (use_pair) {
                 const uint32_t kb = std::clamp<uint32_t>(ceil_log2(grams.size()) + opt.filter_slack, 10, 20);
                 im.key4.assign((size_t(1) << kb) / 32, 0u);
                 for (uint64_t g : grams) {
@@ -599,7 +597,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     im.key4[filter_word(k32, kb - 5)] |= filter_mask_bit(k32);
                 }
             }
-            im.lean_single = lean_single;
             if (use_pair) {
                 im.filter_mode = 2;
                 im.filter = std::move(pair);
@@ -715,7 +712,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                         im.key4[filter_word(h, kb - 5)] |= filter_mask_bit(h);
                     }
                 }
-                im.lean_single = false;
                 std::vector<JumpEntry> entries(keys.size());
                 for (size_t i = 0; i < keys.size(); ++i) {
                     const uint32_t node = knode[i];

@@ -31,7 +31,6 @@ struct GpuImage {
 
     uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
     uint32_t filter_mode = 0; // 0 none, 1 single probe, 2 pair probes (layout.hpp)
-    bool lean_single = false; // single probe, few survivors: two-pass pipeline (filter pass + walking pass)
     uint32_t sym_bits = 0;    // symbol-key mode: bits per packed symbol (filter_mode 3)
     uint32_t pair_shift = 0;
     double filter_pass = 1.0; // estimated fraction of random starts reaching the walk queue
@@ -58,7 +57,6 @@ struct ImageOptions {
     bool jump = true;               // depth-k jump table (HEPFAC_JUMP=0 disables)
     bool jump_ext = true;           // inline pattern lists in the jump table (HEPFAC_JUMP_EXT=0 disables)
     uint32_t filter_mode = 0;       // 0 = cost model, 1 = single, 2 = pair (HEPFAC_FILTER_MODE)
-    bool lean_single = false;       // selective single-probe tries on the two-pass pipeline (HEPFAC_LEAN_SINGLE)
     bool symbol_keys = true;        // packed-symbol filter keys for sigma <= 16 (HEPFAC_SYMBOL_KEYS=0 disables)
 };
 

@@ -1,23 +1,31 @@
-// hepfac_b200_cli -- the reference CLI's end-to-end user path over the B200
-// library: `build` (pattern file -> .htri) and `match` (.htri + input file ->
-// match lines), with the reference's arguments, output formats and exit codes
-// (reference tools/hepfac_cli.cpp:156-193 cmd_build, :234-279 cmd_match,
-// :21-45 exit codes).  Like the reference it talks to the engine only through
-// hepfac.h; the argument parser is hand-written (the reference's CLI11 is not
-// vendored).
+// hepfac_b200_cli -- command-line front end of the B200 library, covering the
+// reference CLI's end-to-end user path (reference tools/hepfac_cli.cpp):
 //
-//   hepfac_b200_cli build --patterns FILE [--sigma N (52)] [--hex] [--compress 0|1|2 (0)] [--out TRIE]
-//   hepfac_b200_cli match --trie TRIE --input FILE [--workers N] [--chunk N] [--depth D] [--out FILE]
+//   build --patterns FILE [--sigma N] [--hex] [--compress 0|1|2] [--out TRIE]
+//         pattern file -> .htri, JSON report (compression stats, memory) on stdout
+//   match --trie TRIE --input FILE [--workers N] [--chunk N] [--depth D] [--out FILE]
+//         "start\tlength\tid" lines (stdout or --out), JSON timing summary on stderr
 //
-// `match` writes "start\tlength\tid" lines to stdout (or --out) and a JSON
-// summary {matches, bytes, seconds, gbps, workers} to stderr.  The lines are
-// byte-identical to the reference's for the same trie and input.
+// Defaults, report fields and exit codes follow the reference (sigma 52,
+// compress 0, out trie.htri; exit 0 ok, 1 invalid input, 2 I/O or format).
+// The match lines are byte-identical to the reference's for the same trie and
+// input.  Everything goes through the public C ABI (hepfac.h).
+//
+// Design: options are declared once in a table (name, takes-value) and parsed
+// into a map; handles are unique_ptrs with the ABI's destroy functions as
+// deleters; the input file is memory-mapped, so the text reaches hepfac_scan
+// as a pageable borrowed pointer (staged by the library's pinned ring) without
+// a read copy; output lines are formatted into one buffer and written once.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cinttypes>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
-#include <cstring>
-#include <fstream>
-#include <iostream>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -26,249 +34,317 @@
 
 namespace {
 
-constexpr int kExitOk = 0;
-constexpr int kExitValidation = 1;
-constexpr int kExitIo = 2;
+enum Exit : int { kOk = 0, kInvalid = 1, kIo = 2 };
 
-int exit_code_for(hepfac_status_t s)
+// Error path: message to stderr, process exit code from the status class.
+struct CliError {
+    int code;
+    std::string message;
+};
+
+Exit exit_class(hepfac_status_t s)
 {
-    if (s == HEPFAC_OK) return kExitOk;
-    if (s == HEPFAC_ERR_IO || s == HEPFAC_ERR_FORMAT) return kExitIo;
-    return kExitValidation;
+    switch (s) {
+    case HEPFAC_OK: return kOk;
+    case HEPFAC_ERR_IO:
+    case HEPFAC_ERR_FORMAT: return kIo;
+    default: return kInvalid;
+    }
 }
 
-[[noreturn]] void fail(hepfac_status_t s, const std::string& context)
+void ok_or_throw(hepfac_status_t s, const char* what)
 {
-    std::cerr << "hepfac: " << context << ": " << hepfac_status_string(s);
+    if (s == HEPFAC_OK) return;
+    std::string m = std::string(what) + ": " + hepfac_status_string(s);
     const char* detail = hepfac_last_error();
-    if (detail && *detail) std::cerr << " (" << detail << ")";
-    std::cerr << "\n";
-    std::exit(exit_code_for(s));
+    if (detail && detail[0]) m += std::string(" (") + detail + ")";
+    throw CliError{exit_class(s), m};
 }
 
-void check(hepfac_status_t s, const std::string& context)
-{
-    if (s != HEPFAC_OK) fail(s, context);
-}
+constexpr const char* kUsage =
+    "usage:\n"
+    "  hepfac_b200_cli build --patterns FILE [--sigma N] [--hex] [--compress 0|1|2] [--out TRIE]\n"
+    "  hepfac_b200_cli match --trie TRIE --input FILE [--workers N] [--chunk N] [--depth D] [--out FILE]\n";
 
-[[noreturn]] void usage(const std::string& why)
-{
-    if (!why.empty()) std::cerr << "hepfac: " << why << "\n";
-    std::cerr << "usage:\n"
-                 "  hepfac_b200_cli build --patterns FILE [--sigma N] [--hex] [--compress 0|1|2] [--out TRIE]\n"
-                 "  hepfac_b200_cli match --trie TRIE --input FILE [--workers N] [--chunk N] [--depth D] "
-                 "[--out FILE]\n";
-    std::exit(kExitValidation);
-}
+[[noreturn]] void bad_usage(const std::string& why) { throw CliError{kInvalid, why + "\n" + kUsage}; }
 
-struct AlphabetHandle {
-    hepfac_alphabet_t* ptr = nullptr;
-    ~AlphabetHandle() { hepfac_alphabet_destroy(ptr); }
-};
-struct PatternsHandle {
-    hepfac_patterns_t* ptr = nullptr;
-    ~PatternsHandle() { hepfac_patterns_destroy(ptr); }
-};
-struct TrieHandle {
-    hepfac_trie_t* ptr = nullptr;
-    ~TrieHandle() { hepfac_trie_destroy(ptr); }
+// ---- options ---------------------------------------------------------------
+
+struct OptionSpec {
+    const char* name;
+    bool value;
 };
 
-std::vector<uint8_t> read_file(const std::string& path)
-{
-    std::ifstream f(path, std::ios::binary | std::ios::ate);
-    if (!f) {
-        std::cerr << "hepfac: cannot open " << path << "\n";
-        std::exit(kExitIo);
-    }
-    std::vector<uint8_t> data(size_t(f.tellg()));
-    f.seekg(0);
-    f.read(reinterpret_cast<char*>(data.data()), std::streamsize(data.size()));
-    if (!f) {
-        std::cerr << "hepfac: read failed: " << path << "\n";
-        std::exit(kExitIo);
-    }
-    return data;
-}
-
-void write_file(const std::string& path, const void* data, size_t size)
-{
-    std::ofstream f(path, std::ios::binary);
-    if (!f || !f.write(static_cast<const char*>(data), std::streamsize(size))) {
-        std::cerr << "hepfac: write failed: " << path << "\n";
-        std::exit(kExitIo);
-    }
-}
-
-uint32_t env_workers()
-{
-    if (const char* env = std::getenv("HEPFAC_WORKERS")) {
-        long v = std::strtol(env, nullptr, 10);
-        if (v >= 1) return uint32_t(v);
-    }
-    return 0;
-}
-
-// --name value pairs and --flags after the subcommand
-struct Args {
-    std::vector<std::pair<std::string, std::string>> kv;
-    std::vector<std::string> flags;
-    bool has(const std::string& k) const
+class Options {
+public:
+    Options(int argc, char** argv, std::initializer_list<OptionSpec> spec)
     {
-        for (auto& p : kv)
-            if (p.first == k) return true;
-        return false;
-    }
-    std::string get(const std::string& k, const std::string& def = "") const
-    {
-        for (auto& p : kv)
-            if (p.first == k) return p.second;
-        return def;
-    }
-    bool flag(const std::string& k) const
-    {
-        for (auto& f : flags)
-            if (f == k) return true;
-        return false;
-    }
-};
-
-Args parse(int argc, char** argv, const std::vector<std::string>& options, const std::vector<std::string>& flag_names)
-{
-    Args a;
-    for (int i = 2; i < argc; ++i) {
-        const std::string s = argv[i];
-        bool known = false;
-        for (auto& f : flag_names)
-            if (s == f) a.flags.push_back(s), known = true;
-        if (known) continue;
-        for (auto& o : options)
-            if (s == o) {
-                if (i + 1 >= argc) usage(s + " needs a value");
-                a.kv.emplace_back(s, argv[++i]);
-                known = true;
+        for (int i = 2; i < argc; ++i) {
+            const std::string tok = argv[i];
+            const OptionSpec* hit = nullptr;
+            for (const auto& s : spec)
+                if (tok == s.name) hit = &s;
+            if (!hit) bad_usage("unknown argument " + tok);
+            if (!hit->value) {
+                values_[tok] = "";
+                continue;
             }
-        if (!known) usage("unknown argument " + s);
+            if (i + 1 == argc) bad_usage(tok + " needs a value");
+            values_[tok] = argv[++i];
+        }
     }
-    return a;
-}
-
-uint64_t to_u64(const std::string& s, const std::string& name)
-{
-    char* end = nullptr;
-    const unsigned long long v = std::strtoull(s.c_str(), &end, 10);
-    if (s.empty() || *end) usage(name + " must be a non-negative integer");
-    return v;
-}
-
-std::string jnum(double v)
-{
-    char b[64];
-    std::snprintf(b, sizeof b, "%.17g", v);
-    return b;
-}
-
-std::string jstr(const std::string& s)
-{
-    std::string o = "\"";
-    for (char c : s) {
-        if (c == '"' || c == '\\') o += '\\';
-        o += c;
+    bool has(const std::string& k) const { return values_.count(k) != 0; }
+    std::string text(const std::string& k, const std::string& fallback = "") const
+    {
+        auto it = values_.find(k);
+        return it == values_.end() ? fallback : it->second;
     }
-    return o + "\"";
+    uint64_t number(const std::string& k, uint64_t fallback) const
+    {
+        auto it = values_.find(k);
+        if (it == values_.end()) return fallback;
+        const std::string& v = it->second;
+        uint64_t x = 0;
+        if (v.empty()) bad_usage(k + " must be a non-negative integer");
+        for (char c : v) {
+            if (c < '0' || c > '9') bad_usage(k + " must be a non-negative integer");
+            x = x * 10 + uint64_t(c - '0');
+        }
+        return x;
+    }
+
+private:
+    std::map<std::string, std::string> values_;
+};
+
+// ---- handles -----------------------------------------------------------------
+
+using AlphabetPtr = std::unique_ptr<hepfac_alphabet_t, decltype(&hepfac_alphabet_destroy)>;
+using PatternsPtr = std::unique_ptr<hepfac_patterns_t, decltype(&hepfac_patterns_destroy)>;
+using TriePtr = std::unique_ptr<hepfac_trie_t, decltype(&hepfac_trie_destroy)>;
+using ListPtr = std::unique_ptr<hepfac_match_list_t, decltype(&hepfac_match_list_destroy)>;
+
+TriePtr no_trie() { return TriePtr(nullptr, &hepfac_trie_destroy); }
+
+// ---- files -------------------------------------------------------------------
+
+// Read-only mapping of a whole file (an empty file maps to nothing).
+class MappedFile {
+public:
+    explicit MappedFile(const std::string& path)
+    {
+        fd_ = ::open(path.c_str(), O_RDONLY);
+        if (fd_ < 0) throw CliError{kIo, "cannot open " + path};
+        struct stat st {};
+        if (::fstat(fd_, &st) != 0) throw CliError{kIo, "cannot stat " + path};
+        size_ = size_t(st.st_size);
+        if (size_) {
+            void* p = ::mmap(nullptr, size_, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd_, 0);
+            if (p == MAP_FAILED) throw CliError{kIo, "cannot map " + path};
+            data_ = static_cast<const uint8_t*>(p);
+        }
+    }
+    ~MappedFile()
+    {
+        if (data_) ::munmap(const_cast<uint8_t*>(data_), size_);
+        if (fd_ >= 0) ::close(fd_);
+    }
+    MappedFile(const MappedFile&) = delete;
+    const uint8_t* data() const { return data_; }
+    size_t size() const { return size_; }
+
+private:
+    int fd_ = -1;
+    const uint8_t* data_ = nullptr;
+    size_t size_ = 0;
+};
+
+void write_all(FILE* f, const std::string& bytes, const std::string& what)
+{
+    if (!bytes.empty() && std::fwrite(bytes.data(), 1, bytes.size(), f) != bytes.size())
+        throw CliError{kIo, "write failed: " + what};
 }
 
-int cmd_build(const Args& a)
-{
-    if (!a.has("--patterns")) usage("build: --patterns is required");
-    const std::string out_path = a.get("--out", "trie.htri");
-    const uint64_t sigma = to_u64(a.get("--sigma", "52"), "--sigma"); // the reference's defaults
-    const uint64_t stages = to_u64(a.get("--compress", "0"), "--compress");
-    if (stages > 2) usage("--compress must be 0, 1 or 2");
-    AlphabetHandle alphabet;
-    check(hepfac_alphabet_standard(uint16_t(sigma), &alphabet.ptr), "alphabet");
-    PatternsHandle patterns;
-    check(hepfac_patterns_load(a.get("--patterns").c_str(), alphabet.ptr, a.flag("--hex") ? 1 : 0, &patterns.ptr),
-          "pattern file");
-    TrieHandle trie;
-    check(hepfac_trie_build(patterns.ptr, &trie.ptr), "trie build");
-    std::string report = "{\n";
-    TrieHandle compressed;
-    const hepfac_trie_t* final_trie = trie.ptr;
-    if (stages > 0) {
-        hepfac_compression_stats_t st{};
-        check(hepfac_trie_compress_stats(trie.ptr, int(stages), &compressed.ptr, &st), "compression");
-        final_trie = compressed.ptr;
-        report += "  \"compression\": {\n    \"nodes_before\": " + std::to_string(st.nodes_before) +
-                  ",\n    \"nodes_after_stage1\": " + std::to_string(st.nodes_after_stage1) +
-                  ",\n    \"nodes_after_stage2\": " + std::to_string(st.nodes_after_stage2) +
-                  ",\n    \"pattern_count\": " + std::to_string(st.pattern_count) +
-                  ",\n    \"reduction_percent\": " + jnum(st.reduction_percent) + "\n  },\n";
+// ---- JSON (the two small reports) ---------------------------------------------
+
+// Pretty: one key per line, two spaces per level (the build report);
+// compact: one line (the match summary).
+class Json {
+public:
+    explicit Json(bool pretty) : pretty_(pretty) {}
+    Json& open() { return raw("{"), first_ = true, *this; }
+    Json& close(int indent) { return newline(indent - 2), raw("}"), first_ = false, *this; }
+    Json& key(const char* k, int indent)
+    {
+        if (!first_) raw(",");
+        first_ = false;
+        newline(indent);
+        return raw("\""), raw(k), raw(pretty_ ? "\": " : "\":");
     }
-    check(hepfac_trie_save(final_trie, out_path.c_str()), "trie save");
+    Json& num(uint64_t v) { return raw(std::to_string(v)); }
+    Json& real(double v)
+    {
+        char b[40];
+        std::snprintf(b, sizeof b, "%.17g", v);
+        return raw(b);
+    }
+    Json& str(const std::string& s)
+    {
+        raw("\"");
+        for (char c : s) {
+            if (c == '"' || c == '\\') out_ += '\\';
+            out_ += c;
+        }
+        return raw("\"");
+    }
+    const std::string& text() const { return out_; }
+
+private:
+    Json& raw(const std::string& s) { return out_ += s, *this; }
+    void newline(int indent)
+    {
+        if (pretty_) out_ += "\n" + std::string(size_t(indent), ' ');
+    }
+    std::string out_;
+    bool pretty_;
+    bool first_ = true;
+};
+
+// ---- subcommands ---------------------------------------------------------------
+
+int run_build(const Options& o)
+{
+    if (!o.has("--patterns")) bad_usage("build: --patterns is required");
+    const std::string out = o.text("--out", "trie.htri");
+    const uint64_t sigma = o.number("--sigma", 52);
+    const uint64_t stages = o.number("--compress", 0);
+    if (stages > 2) bad_usage("--compress must be 0, 1 or 2");
+
+    hepfac_alphabet_t* a = nullptr;
+    ok_or_throw(hepfac_alphabet_standard(uint16_t(sigma), &a), "alphabet");
+    AlphabetPtr alphabet(a, &hepfac_alphabet_destroy);
+    hepfac_patterns_t* p = nullptr;
+    ok_or_throw(hepfac_patterns_load(o.text("--patterns").c_str(), alphabet.get(), o.has("--hex") ? 1 : 0, &p),
+                "pattern file");
+    PatternsPtr patterns(p, &hepfac_patterns_destroy);
+    hepfac_trie_t* t = nullptr;
+    ok_or_throw(hepfac_trie_build(patterns.get(), &t), "trie build");
+    TriePtr trie(t, &hepfac_trie_destroy);
+
+    Json j(true);
+    j.open();
+    if (stages) {
+        hepfac_compression_stats_t cs{};
+        hepfac_trie_t* c = nullptr;
+        ok_or_throw(hepfac_trie_compress_stats(trie.get(), int(stages), &c, &cs), "compression");
+        trie.reset(c);
+        j.key("compression", 2).open();
+        j.key("nodes_before", 4).num(cs.nodes_before);
+        j.key("nodes_after_stage1", 4).num(cs.nodes_after_stage1);
+        j.key("nodes_after_stage2", 4).num(cs.nodes_after_stage2);
+        j.key("pattern_count", 4).num(cs.pattern_count);
+        j.key("reduction_percent", 4).real(cs.reduction_percent);
+        j.close(4);
+    }
+    ok_or_throw(hepfac_trie_save(trie.get(), out.c_str()), "trie save");
     hepfac_memory_report_t mem{};
-    check(hepfac_trie_memory_report(final_trie, &mem), "memory report");
-    report += "  \"memory\": {\n    \"node_count\": " + std::to_string(mem.node_count) +
-              ",\n    \"bytes_per_node\": " + std::to_string(mem.bytes_per_node) +
-              ",\n    \"total_bytes\": " + std::to_string(mem.total_bytes) + ",\n    \"total_mib\": " +
-              jstr(mem.total_mib) + ",\n    \"sigma\": " + std::to_string(mem.sigma) + "\n  },\n  \"trie\": " +
-              jstr(out_path) + "\n}\n";
-    std::cout << report;
-    return kExitOk;
+    ok_or_throw(hepfac_trie_memory_report(trie.get(), &mem), "memory report");
+    j.key("memory", 2).open();
+    j.key("node_count", 4).num(mem.node_count);
+    j.key("bytes_per_node", 4).num(mem.bytes_per_node);
+    j.key("total_bytes", 4).num(mem.total_bytes);
+    j.key("total_mib", 4).str(mem.total_mib);
+    j.key("sigma", 4).num(mem.sigma);
+    j.close(4);
+    j.key("trie", 2).str(out);
+    j.close(2);
+    write_all(stdout, j.text() + "\n", "stdout");
+    return kOk;
 }
 
-int cmd_match(const Args& a)
+int run_match(const Options& o)
 {
-    if (!a.has("--trie") || !a.has("--input")) usage("match: --trie and --input are required");
-    const uint32_t workers = a.has("--workers") ? uint32_t(to_u64(a.get("--workers"), "--workers")) : env_workers();
-    const uint32_t chunk = uint32_t(to_u64(a.get("--chunk", "0"), "--chunk"));
-    const uint32_t depth = uint32_t(to_u64(a.get("--depth", "0"), "--depth"));
-    TrieHandle loaded;
-    check(hepfac_trie_load(a.get("--trie").c_str(), &loaded.ptr), "trie load");
-    TrieHandle truncated;
-    const hepfac_trie_t* trie = loaded.ptr;
-    if (depth > 0) {
+    if (!o.has("--trie") || !o.has("--input")) bad_usage("match: --trie and --input are required");
+    uint64_t workers = o.number("--workers", 0);
+    if (!o.has("--workers"))
+        if (const char* env = std::getenv("HEPFAC_WORKERS")) workers = std::strtoull(env, nullptr, 10);
+    const hepfac_scan_config_t config{uint32_t(workers), uint32_t(o.number("--chunk", 0))};
+    const uint64_t depth = o.number("--depth", 0);
+
+    hepfac_trie_t* t = nullptr;
+    ok_or_throw(hepfac_trie_load(o.text("--trie").c_str(), &t), "trie load");
+    TriePtr trie(t, &hepfac_trie_destroy), truncated = no_trie();
+    if (depth) {
+        hepfac_trie_t* d = nullptr;
         int noop = 0;
-        check(hepfac_trie_truncate(loaded.ptr, depth, &truncated.ptr, &noop), "truncate");
-        trie = truncated.ptr;
+        ok_or_throw(hepfac_trie_truncate(trie.get(), uint32_t(depth), &d, &noop), "truncate");
+        truncated.reset(d);
     }
-    std::vector<uint8_t> text = read_file(a.get("--input"));
-    hepfac_scan_config_t config{workers, chunk};
+    const hepfac_trie_t* active = truncated ? truncated.get() : trie.get();
+    const MappedFile input(o.text("--input"));
 
+    // one timed run first (the reference reports run_throughput's figures;
+    // it refuses an empty corpus, so an empty input reports zeros)
     hepfac_throughput_report_t rep{};
-    if (!text.empty()) // the reference's run_throughput refuses an empty corpus
-        check(hepfac_run_throughput(trie, text.data(), text.size(), &config, 1, &rep), "throughput");
+    if (input.size())
+        ok_or_throw(hepfac_run_throughput(active, input.data(), input.size(), &config, 1, &rep), "throughput");
+    hepfac_match_list_t* l = nullptr;
+    ok_or_throw(hepfac_scan(active, input.data(), input.size(), &config, &l), "scan");
+    const ListPtr list(l, &hepfac_match_list_destroy);
 
-    hepfac_match_list_t* list = nullptr;
-    check(hepfac_scan(trie, text.data(), text.size(), &config, &list), "scan");
-    std::unique_ptr<hepfac_match_list_t, decltype(&hepfac_match_list_destroy)> guard(list,
-                                                                                      &hepfac_match_list_destroy);
-    const hepfac_match_t* data = hepfac_match_list_data(list);
-    const size_t n = hepfac_match_list_size(list);
+    const size_t n = hepfac_match_list_size(list.get());
+    const hepfac_match_t* m = hepfac_match_list_data(list.get());
     std::string lines;
-    lines.reserve(n * 24);
-    char buf[96];
-    for (size_t i = 0; i < n; ++i) {
-        const int k = std::snprintf(buf, sizeof buf, "%llu\t%u\t%u\n", (unsigned long long)data[i].start,
-                                    data[i].length, data[i].pattern_id);
-        lines.append(buf, size_t(k));
+    lines.resize(n * 43 + 1); // u64 (20 digits) + two u32 (10), two tabs, newline; + sprintf's NUL
+    char* w = lines.data();
+    for (size_t i = 0; i < n; ++i)
+        w += std::sprintf(w, "%" PRIu64 "\t%" PRIu32 "\t%" PRIu32 "\n", m[i].start, m[i].length, m[i].pattern_id);
+    lines.resize(size_t(w - lines.data()));
+    if (o.has("--out")) {
+        const std::string path = o.text("--out");
+        FILE* f = std::fopen(path.c_str(), "wb");
+        if (!f) throw CliError{kIo, "cannot open " + path};
+        const std::unique_ptr<FILE, int (*)(FILE*)> closer(f, &std::fclose);
+        write_all(f, lines, path);
+    } else {
+        write_all(stdout, lines, "stdout");
     }
-    if (a.has("--out")) write_file(a.get("--out"), lines.data(), lines.size());
-    else std::cout << lines;
-    // timing goes to stderr so the match list stays byte-identical across runs
-    std::cerr << "{\"matches\":" << n << ",\"bytes\":" << rep.bytes << ",\"seconds\":" << jnum(rep.seconds)
-              << ",\"gbps\":" << jnum(rep.gbps) << ",\"workers\":" << rep.workers << "}\n";
-    return kExitOk;
+    // timing on stderr, so the match lines stay byte-identical across runs
+    Json j(false);
+    j.open();
+    j.key("matches", 0).num(n);
+    j.key("bytes", 0).num(rep.bytes);
+    j.key("seconds", 0).real(rep.seconds);
+    j.key("gbps", 0).real(rep.gbps);
+    j.key("workers", 0).num(rep.workers);
+    j.close(2);
+    std::fprintf(stderr, "%s\n", j.text().c_str());
+    return kOk;
 }
 
 } // namespace
 
 int main(int argc, char** argv)
 {
-    if (argc < 2) usage("");
-    const std::string cmd = argv[1];
-    if (cmd == "build") return cmd_build(parse(argc, argv, {"--patterns", "--sigma", "--compress", "--out"}, {"--hex"}));
-    if (cmd == "match")
-        return cmd_match(parse(argc, argv, {"--trie", "--input", "--workers", "--chunk", "--depth", "--out"}, {}));
-    usage("unknown subcommand " + cmd);
+    try {
+        if (argc < 2) bad_usage("missing subcommand");
+        const std::string sub = argv[1];
+        if (sub == "build")
+            return run_build(Options(argc, argv, {{"--patterns", true},
+                                                  {"--sigma", true},
+                                                  {"--compress", true},
+                                                  {"--out", true},
+                                                  {"--hex", false}}));
+        if (sub == "match")
+            return run_match(Options(argc, argv, {{"--trie", true},
+                                                  {"--input", true},
+                                                  {"--workers", true},
+                                                  {"--chunk", true},
+                                                  {"--depth", true},
+                                                  {"--out", true}}));
+        bad_usage("unknown subcommand " + sub);
+    } catch (const CliError& e) {
+        std::fprintf(stderr, "hepfac: %s\n", e.message.c_str());
+        return e.code;
+    }
 }

@@ -338,22 +338,6 @@ def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth):
     assert same(got, oracle.naive_find_all(tx, pats))
 
 
-@pytest.mark.parametrize("stages,depth", [(1, 5), (2, None)])
-def test_lean_single_pipeline(gpu, monkeypatch, stages, depth):
-    # the opt-in single-probe two-pass pipeline (HEPFAC_LEAN_SINGLE=1, k >= 4)
-    monkeypatch.setenv("HEPFAC_LEAN_SINGLE", "1")
-    monkeypatch.setenv("HEPFAC_FILTER_MODE", "single")
-    monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
-    rng = np.random.default_rng(33)
-    a, syms = alphabet_bytes(gpu, 20)
-    pats = pattern_set(rng, syms, 2000, 6, 20)
-    t = build(gpu, pats, 20, stages, depth)
-    tx = text(rng, syms, 1 << 20)
-    for i, p in enumerate(pats):
-        plant(tx, p, (i * 331) % (tx.size - 24))
-    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
-
-
 @pytest.mark.parametrize("ext", ["1", "0"])
 @pytest.mark.parametrize("two_pass", [False, True])
 @pytest.mark.parametrize("sigma,depth", [(4, 8), (20, 5), (256, 4)])
