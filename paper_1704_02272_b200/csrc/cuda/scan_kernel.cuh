@@ -695,7 +695,8 @@ struct Walker {
                     off = q[e];
                     keep = probe2<KW>(a, lo + off);
                 }
-                const uint32_t b = __ballot_sync(0xFFFFFFFFu, keep); // every read of this round is done
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, keep);
+                __syncwarp(); // every read of this round is done (and ordered) before the in-place writes
                 if (keep) q[ns + __popc(b & below)] = off;          // compaction in place, order kept
                 ns += __popc(b);
             }
