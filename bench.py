@@ -353,12 +353,17 @@ def main():
     e2e_steps = args.e2e_steps or min(args.steps, 5)
 
     def e2e_run(buf):
+        # view=True: the records stay in the library's (pinned) list, as a C
+        # caller gets them -- no extra host copy by the Python binding
+        r = None
         for _ in range(min(args.warmup, 2)):
-            r = lib.scan_shard(trie, buf, lo, owned)
+            r = None
+            r = lib.scan_shard(trie, buf, lo, owned, view=True)
         d.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            r = lib.scan_shard(trie, buf, lo, owned)
+            r = None  # the previous list goes back to the pinned pool first
+            r = lib.scan_shard(trie, buf, lo, owned, view=True)
             d.exclusive_prefix(int(r.size))
         d.barrier()
         return r, d.max(time.perf_counter() - t0), lib.last_scan_stats()

@@ -1025,9 +1025,12 @@ bool is_pageable(const void* p)
 uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, uint64_t avail, uint64_t owned,
                      uint64_t g0, uint64_t halo, MatchList* sink, ScanStats& st)
 {
-    const uint64_t C = stream_chunk_bytes();
-    const uint64_t n = (owned + C - 1) / C;
     const bool stage = is_pageable(text);
+    // Staged (pageable) text: at least ~8 chunks of >= 4 MiB, so the host
+    // copy of chunk c+1 overlaps the DMA of chunk c even for small texts.
+    uint64_t C = stream_chunk_bytes();
+    if (stage) C = std::min(C, std::max<uint64_t>(uint64_t(4) << 20, ((owned + 7) / 8 + 0xFFFFF) & ~uint64_t(0xFFFFF)));
+    const uint64_t n = (owned + C - 1) / C;
     const uint64_t slot_bytes = std::min(avail, C + halo);
     ws.ensure_slots(slot_bytes);
     if (stage) ws.ensure_staging(slot_bytes);

@@ -264,9 +264,19 @@ class Library:
         return buf.value.decode()
 
     # -- matching ---------------------------------------------------------
-    def _list(self, h) -> np.ndarray:
+    def _list(self, h, view: bool = False) -> np.ndarray:
+        """The records of a match list.  view=False copies them and destroys
+        the list; view=True returns a zero-copy array over the list's own
+        memory (hepfac_match_list_data), which destroys the list when the
+        array (and every view of it) is garbage-collected -- what a C caller
+        gets, without a host copy of the records."""
+        n = self.dll.hepfac_match_list_size(h)
+        if view and n:
+            import weakref
+            buf = (C.c_uint8 * (n * MATCH_DTYPE.itemsize)).from_address(self.dll.hepfac_match_list_data(h))
+            weakref.finalize(buf, self.dll.hepfac_match_list_destroy, h)
+            return np.frombuffer(buf, dtype=MATCH_DTYPE)
         try:
-            n = self.dll.hepfac_match_list_size(h)
             out = np.empty(n, dtype=MATCH_DTYPE)
             if n:
                 C.memmove(out.ctypes.data, self.dll.hepfac_match_list_data(h), n * MATCH_DTYPE.itemsize)
@@ -274,13 +284,14 @@ class Library:
         finally:
             self.dll.hepfac_match_list_destroy(h)
 
-    def scan(self, trie: "Trie", text, workers: int = 0, chunk: int = 0) -> np.ndarray:
-        """hepfac_scan: every occurrence sorted by (start, length, pattern_id)."""
+    def scan(self, trie: "Trie", text, workers: int = 0, chunk: int = 0, view: bool = False) -> np.ndarray:
+        """hepfac_scan: every occurrence sorted by (start, length, pattern_id)
+        (view=True: zero-copy over the library's list, see _list)."""
         arr = _as_u8(text)
         cfg = _ScanConfig(workers, chunk)
         h = C.c_void_p()
         self.check(self.dll.hepfac_scan(trie.h, _ptr(arr), arr.size, C.byref(cfg), C.byref(h)))
-        return self._list(h)
+        return self._list(h, view)
 
     def scan_two_stage(self, trie: "Trie", text, workers: int = 0, chunk: int = 0) -> np.ndarray:
         """Reference scan_two_stage (scan.cpp:121-129): a scan that requires a truncated trie."""
@@ -317,11 +328,11 @@ class Library:
         self.check(self.dll.hepfac_b200_halo(trie.h, C.byref(v)))
         return None if v.value == (1 << 64) - 1 else v.value
 
-    def scan_shard(self, trie: "Trie", text, offset: int, owned: int) -> np.ndarray:
+    def scan_shard(self, trie: "Trie", text, offset: int, owned: int, view: bool = False) -> np.ndarray:
         arr = _as_u8(text)
         h = C.c_void_p()
         self.check(self.dll.hepfac_b200_scan_shard(trie.h, _ptr(arr), arr.size, offset, owned, C.byref(h)))
-        return self._list(h)
+        return self._list(h, view)
 
     def last_scan_stats(self) -> dict:
         s = _ScanStats()
