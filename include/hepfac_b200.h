@@ -96,7 +96,8 @@ typedef struct hepfac_b200_layout_info {
     uint64_t device_bytes;
     uint64_t private_terminals;
     uint64_t keyed_terminals;
-    uint32_t filter_mode;     /* 0 none, 1 single probe per start, 2 pair probes (one per two starts) */
+    uint32_t filter_mode;     /* 0 none, 1 single probe per start, 2 pair probes (one per two starts),
+                                 3 packed-symbol keys, 4 single probe + L2-resident bitmap (two-pass) */
     uint32_t filter_pass_ppm; /* estimated random starts per million that reach the walk queue */
 } hepfac_b200_layout_info_t;
 

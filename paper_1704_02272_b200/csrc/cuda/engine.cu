@@ -259,6 +259,7 @@ struct DeviceTrie {
     bool grouped = false, identity = false;
     int kw = 0;
     bool pair = false;          // two-pass pipeline: filter pass + candidate-walking pass
+    uint32_t filter_mode = 0;   // image.cpp: 1 single, 2 pair, 3 packed symbols, 4 single + L2 bitmap
     void (*filter_fn)(gpu::FilterArgs) = nullptr;
     double filter_pass = 1.0;
     KernelFn kernel = nullptr;
@@ -413,7 +414,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     // two-pass pipeline (always for symbol keys: the one-pass kernel reads byte keys)
     d->sym_bits = im.sym_bits;
-    d->pair = (im.filter_mode == 2 && pair_pipeline_enabled()) || im.filter_mode == 3;
+    d->pair = ((im.filter_mode == 2 || im.filter_mode == 4) && pair_pipeline_enabled()) || im.filter_mode == 3;
+    d->filter_mode = im.filter_mode;
     if (d->pair) {
         d->pipeline_min = im.filter_mode == 3 ? 0 : pipeline_min_bytes();
         if (im.filter_mode == 3) {
@@ -424,7 +426,10 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                                           : (im.sym_bits == 2 ? gpu::pfac_pack_symbols_kernel<2>
                                                               : gpu::pfac_pack_symbols_kernel<4>);
         } else {
-            d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_kernel : gpu::pfac_pair_filter2_kernel;
+            if (im.filter_mode == 4)
+                d->filter_fn = d->kw == 3 ? gpu::pfac_l2_filter_kernel<3> : gpu::pfac_l2_filter_kernel<2>;
+            else
+                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_kernel : gpu::pfac_pair_filter2_kernel;
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
@@ -433,7 +438,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                                                          int(gpu::kCWarps * 32), d->walk_smem));
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         d->filter_smem = size_t(v.filter_words) * 4 +
-                         (im.filter_mode == 3
+                         ((im.filter_mode == 3 || im.filter_mode == 4)
                               ? 0
                               : (pair_queue_form() ? gpu::filter_smem_fixed_bytes() : gpu::filter2_smem_fixed_bytes()));
         allow_max_smem(d->filter_fn, device);
@@ -809,6 +814,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.tile_cslot = ws.d_tile_cslot;
         f.cand_need = ws.d_small + 5;
         f.filter_k = dt.view.filter_k;
+        f.table2 = dt.view.filter2;
+        f.table2_bits = dt.view.filter2_bits;
         if (dt.sym_bits) {
             const uint64_t per = 32 / dt.sym_bits, words = (n_avail + per - 1) / per;
             ws.regrow(ws.d_packed, ws.packed_cap, words + 4);
@@ -822,6 +829,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
         CK(cudaGetLastError());
         if (between) CK(cudaEventRecord(between, ws.stream));
+        // the single + L2 filter pass already tested the L2 bitmap
+        if (dt.filter_mode == 4) a.trie.filter2_bits = 0;
         a.cand = ws.d_cand;
         a.cand_key = ws.d_cand_key;
         a.cand_cap = ws.cand_cap;
@@ -1317,7 +1326,7 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
-    li.filter_mode = d->kw == 0 ? 0u : (d->sym_bits ? 3u : (d->pair ? 2u : 1u));
+    li.filter_mode = d->kw == 0 ? 0u : d->filter_mode;
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }

@@ -58,8 +58,10 @@ struct FilterArgs {
     uint32_t* tile_ccount;
     uint32_t* tile_cslot;
     unsigned long long* cand_need; // max entries any warp needed (overflow sizing)
-    // symbol form: k symbols per key
+    // symbol form: k symbols per key; single + L2 form: k bytes
     uint32_t filter_k;
+    const uint32_t* table2;  // single + L2 form: the 2^table2_bits-bit bitmap in global memory
+    uint32_t table2_bits;
     const uint32_t* packed;  // symbol form: the text packed by pfac_pack_symbols_kernel
 };
 
@@ -448,6 +450,129 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const _
         if (lane == 0) {
             a.tile_ccount[tile] = cursor - slot;
             a.tile_cslot[tile] = uint32_t(slot);
+        }
+    }
+    if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
+}
+
+// ---- single probe + L2 bitmap (large dictionaries) --------------------------------
+//
+// For dictionaries whose k-gram set saturates any shared-memory bitmap (c5 at
+// 1M patterns: 2^20 bits for ~1M keys pass 61% of random starts), the filter
+// pass tests every start against both levels of the single-probe filter
+// (layout.hpp): the shared-memory bitmap and the 2^filter2_bits-bit bitmap in
+// global memory (16 MiB, L2-resident).  All 16 L2 probes of a lane slice are
+// issued before the first is tested (predicated on the first level), so a
+// warp has up to 512 L2 loads in flight instead of one dependent chain per
+// start; survivors (~1% at 1M patterns) go to the walking pass.
+// Key of start j (KW 3: k == 4, KW 2: k in 5..8): the same fold as the host's
+// filter_fold.  w[0..5] = the slice's 16 bytes and the next 8.
+template <int KW>
+__device__ __forceinline__ uint32_t f_key(const uint32_t (&w)[6], int j, uint32_t mhi)
+{
+    const uint32_t lo = (j & 3) ? __funnelshift_r(w[j >> 2], w[(j >> 2) + 1], 8 * (j & 3)) : w[j >> 2];
+    if (KW != 2) return lo;
+    const uint32_t hi = ((j & 3) ? __funnelshift_r(w[(j >> 2) + 1], w[(j >> 2) + 2], 8 * (j & 3)) : w[(j >> 2) + 1]) & mhi;
+    return lo + hi * 0x85EBCA77u; // filter_fold
+}
+
+template <int KW>
+__global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __grid_constant__ FilterArgs a)
+{
+    extern __shared__ __align__(128) uint8_t fsmem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
+    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
+    __syncthreads();
+    const uint8_t* tbytes = fsmem;
+    const uint32_t mask4 = (a.table_words - 1u) << 2;
+    const uint32_t k = a.filter_k;
+    const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
+    const uint32_t* l2 = a.table2;
+    const uint32_t sh2 = 32u - a.table2_bits;
+
+    const uint32_t gw = blockIdx.x * kFWarps + (tid >> 5), W = gridDim.x * kFWarps;
+    const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
+    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
+    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
+    const uint32_t cap = uint32_t(min(a.cand_cap, uint64_t(0xFFFFFFFFu)));
+    uint32_t cursor = 0;
+    const uint32_t below = (1u << lane) - 1u;
+    auto load = [&](uint64_t at) -> uint4 {
+        const uint64_t p = at + 16u * lane;
+        return p < avail16 ? __ldg(reinterpret_cast<const uint4*>(a.text + p)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+
+    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
+        const uint64_t lo = tile * kFTile;
+        const uint32_t slot = cursor;
+        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
+        const uint32_t chunks = (rem + kFChunk - 1) / kFChunk;
+        uint4 nxt = chunks ? load(lo) : make_uint4(0u, 0u, 0u, 0u);
+        for (uint32_t c = 0; c < chunks; ++c) {
+            const uint64_t cbase = lo + uint64_t(c) * kFChunk;
+            const uint4 cur = nxt;
+            if (c + 1 < chunks) nxt = load(cbase + kFChunk);
+            // the 8 bytes after the slice: the next lane's first 8, lane 31's
+            // from the next chunk (its first lane's load, or memory)
+            uint32_t ox = __shfl_sync(0xFFFFFFFFu, cur.x, (lane + 1) & 31u);
+            uint32_t oy = __shfl_sync(0xFFFFFFFFu, cur.y, (lane + 1) & 31u);
+            const uint32_t nx = __shfl_sync(0xFFFFFFFFu, nxt.x, 0), ny = __shfl_sync(0xFFFFFFFFu, nxt.y, 0);
+            if (lane == 31) {
+                if (c + 1 < chunks) {
+                    ox = nx, oy = ny;
+                } else {
+                    const uint64_t p = cbase + kFChunk;
+                    const uint2 t = p < avail16 ? __ldg(reinterpret_cast<const uint2*>(a.text + p)) : make_uint2(0u, 0u);
+                    ox = t.x, oy = t.y;
+                }
+            }
+            const uint32_t w[6] = {cur.x, cur.y, cur.z, cur.w, ox, oy};
+            const int32_t r = int32_t(rem) - int32_t(c * kFChunk + 16u * lane);
+            const uint32_t valid = r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
+            // level 1 (shared memory) for the 16 starts, then every level-2
+            // probe in flight before the first test
+            uint32_t m = 0, w2[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t key = f_key<KW>(w, j, mhi);
+                const uint32_t word = *reinterpret_cast<const uint32_t*>(tbytes + (__umulhi(key, kFilterMul) & mask4));
+                const bool hit = ((valid >> j) & 1u) && int32_t(word << (key & 31u)) < 0;
+                const uint32_t s2 = filter2_hash(key) >> sh2;
+                w2[j] = hit ? __ldg(l2 + (s2 >> 5)) >> (s2 & 31u) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) m |= (w2[j] & 1u) << j;
+            if (!__any_sync(0xFFFFFFFFu, m)) continue;
+            // survivors in start order (chunk, lane, j)
+            const uint32_t n = __popc(m);
+            uint32_t at;
+            if (!__any_sync(0xFFFFFFFFu, n > 1)) {
+                at = cursor + __popc(__ballot_sync(0xFFFFFFFFu, n != 0) & below);
+            } else {
+                uint32_t incl = n;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                    if (lane >= uint32_t(d)) incl += u;
+                }
+                at = cursor + incl - n;
+            }
+            const uint32_t first = c * kFChunk + 16u * lane; // tile offset of the slice
+            for (uint32_t x = m; x; x &= x - 1, ++at) {
+                const int j = __ffs(x) - 1;
+                if (at < cap) { // (rare: re-read the first 4 bytes rather than index w[] dynamically)
+                    const uint64_t pos = lo + first + uint32_t(j);
+                    const uint32_t* tp = reinterpret_cast<const uint32_t*>(a.text + (pos & ~3ull));
+                    region[at] = uint16_t(first + j);
+                    keys[at] = __funnelshift_r(__ldg(tp), __ldg(tp + 1), 8u * uint32_t(pos & 3u));
+                }
+            }
+            cursor += __reduce_add_sync(0xFFFFFFFFu, n);
+        }
+        if (lane == 0) {
+            a.tile_ccount[tile] = cursor - slot;
+            a.tile_cslot[tile] = slot;
         }
     }
     if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);

@@ -49,7 +49,7 @@ ImageOptions image_options_from_env()
     if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
         const std::string m = s;
-        o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : 0u);
+        o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : (m == "l2" ? 4u : 0u));
     }
     if (const char* s = std::getenv("HEPFAC_FILTER2_SLACK")) {
         long v = std::strtol(s, nullptr, 10);
@@ -582,7 +582,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             bool use_pair = k >= 4 && cost_pair < cost_single;
             f_single = p_single;
             f_pair = std::sqrt(p_both);
-            if (opt.filter_mode == 1) use_pair = false;
+            if (opt.filter_mode == 1 || opt.filter_mode == 4) use_pair = false;
             if (opt.filter_mode == 2) use_pair = k >= 4;
             // Two-pass pipeline (lean filter pass, then the walking pass) for
             // the pair form: the walking pass re-checks survivors' first 4
@@ -624,6 +624,16 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     const uint32_t s2 = filter2_slot(filter_fold(g), bits2);
                     im.filter2[s2 >> 5] |= 1u << (s2 & 31);
                 }
+            }
+            // Saturated first level (dictionaries of ~10^6 k-grams: 2^20 bits
+            // in shared memory pass most random starts): the two-pass
+            // pipeline with a filter pass that tests both levels for every
+            // start (pfac_l2_filter_kernel), instead of the fused kernel's
+            // one dependent L2 probe chain per survivor.
+            if (im.filter_mode == 1 && k >= 4 && im.filter2_bits &&
+                (opt.filter_mode == 4 || (opt.filter_mode == 0 && p_single > 0.25))) {
+                im.filter_mode = 4;
+                im.filter_pass = p_single * double(popcount(im.filter2)) / double(uint64_t(1) << im.filter2_bits);
             }
             if (opt.jump) {
                 std::vector<JumpEntry> entries(grams.size());

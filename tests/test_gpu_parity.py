@@ -319,25 +319,46 @@ def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth, t
 
 
 @pytest.mark.parametrize("stages,depth", [(1, 4), (2, None)])
-def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth):
-    # Every start of a run of 'A's passes both pair levels and the prefix
+@pytest.mark.parametrize("mode,code", [("pair", 2), ("l2", 4)])
+def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth, mode, code):
+    # Every start of a run of 'A's passes both filter levels and the prefix
     # recheck: exercises the filter pass's per-chunk fallback (a step with more
     # candidates than its queue), candidate-region overflow and re-run, and
-    # walk units with more candidates than a warp queue.
-    monkeypatch.setenv("HEPFAC_FILTER_MODE", "pair")
+    # walk units with more candidates than a warp queue.  Both two-pass filter
+    # forms: pair probes, and the single probe + L2 bitmap.
+    monkeypatch.setenv("HEPFAC_FILTER_MODE", mode)
     monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
     rng = np.random.default_rng(31)
     syms = np.arange(256, dtype=np.uint8)
     pats = pattern_set(rng, syms, 1000, 4, 24)
     pats = sorted(set(pats) | {b"AAAA", b"AAAAB", b"AAAAAAAA", b"AAAAAAAAAAAAAAAAAAAAAAAAAAAAAA"})
     t = build(gpu, pats, 256, stages, depth)
-    assert gpu.layout_info(t)["filter_mode"] == 2
+    assert gpu.layout_info(t)["filter_mode"] == code
     tx = np.frombuffer(b"A" * 400000, dtype=np.uint8).copy()
     tx[123456:123456 + 4096] = text(rng, syms, 4096)
     for i, p in enumerate(pats[:200]):
         plant(tx, p, 200000 + i * 97)
     got = gpu.scan(t, tx)
     assert same(got, oracle.naive_find_all(tx, pats))
+
+
+@pytest.mark.parametrize("sigma,lo", [(20, 5), (64, 4), (256, 4), (256, 7)])
+@pytest.mark.parametrize("stages,depth", [(0, None), (1, 6), (2, None)])
+def test_l2_filter_pipeline_random(gpu, monkeypatch, sigma, lo, stages, depth):
+    # The single probe + L2 bitmap filter pass (filter mode 4, chosen by the
+    # image builder when the shared-memory level saturates: c5 at 1M
+    # patterns) on random instances, k = 4 and k in 5..8, every trie state.
+    monkeypatch.setenv("HEPFAC_FILTER_MODE", "l2")
+    monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
+    rng = np.random.default_rng(sigma * 13 + lo + stages)
+    a, syms = alphabet_bytes(gpu, sigma)
+    pats = pattern_set(rng, syms, 1500, lo, 30)
+    t = build(gpu, pats, sigma, stages, depth)
+    assert gpu.layout_info(t)["filter_mode"] == 4
+    tx = text(rng, syms, (1 << 21) + 333)
+    for i in range(0, tx.size - 40, 1499):
+        plant(tx, pats[i % len(pats)], i)
+    assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats))
 
 
 @pytest.mark.parametrize("ext", ["1", "0"])
