@@ -21,6 +21,7 @@
 
 #include "../host/image.hpp"
 #include "engine.hpp"
+#include "dna_kernel.cuh"
 #include "filter_kernel.cuh"
 #include "scan_kernel.cuh"
 
@@ -275,6 +276,11 @@ struct DeviceTrie {
     uint32_t sym_bits = 0; // symbol-key mode: the text is packed before the filter pass
     void (*pack_fn)(const uint8_t*, uint64_t, const uint16_t*, uint32_t*) = nullptr;
     int blocks_per_sm = 1, sm_count = 1;
+    // direct-index mode (filter mode 5): pack pass + pfac_dna_kernel
+    bool dna = false;
+    KernelFn dna_kernel = nullptr;
+    size_t dna_smem = 0;
+    uint32_t dna_warps = 0;
     uint32_t warps = gpu::kWarps; // per CTA of `kernel`
     uint32_t min_emit = UINT32_MAX, node_count = 0, groups = 0;
     uint64_t reach = 0, filter_paths = 0, device_bytes = 0, private_terminals = 0, keyed_terminals = 0;
@@ -405,6 +411,24 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.jump_bits = im.jump_bits;
     v.jump_ext = im.jump_ext.empty() ? nullptr : d->upload(im.jump_ext);
     v.min_emit = im.min_emit;
+    if (im.filter_mode == 5) {
+        v.dna = d->upload(im.dna);
+        v.dna_words = uint32_t(im.dna.size());
+        v.dna_keys = im.dna_keys;
+        v.dna_pats = im.dna_pats;
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        // 32 warps when the tables and 32 queues fit next to the static
+        // shared memory, else 16
+        const bool wide = gpu::dna_smem_bytes(im.dna_keys, im.dna_pats, 32) + 1024 <= size_t(optin);
+        d->dna_warps = wide ? 32u : 16u;
+        d->dna_kernel = wide ? gpu::pfac_dna_kernel<32> : gpu::pfac_dna_kernel<16>;
+        d->dna_smem = gpu::dna_smem_bytes(im.dna_keys, im.dna_pats, d->dna_warps);
+        allow_max_smem(d->dna_kernel, device);
+        int bps = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, d->dna_kernel, int(d->dna_warps * 32), d->dna_smem));
+        d->dna = bps >= 1;
+    }
 
     // one-pass (fused) kernel: always available
     d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
@@ -748,7 +772,8 @@ Launch plan(const DeviceTrie& dt, uint64_t n_own)
         l.n_ftiles = l.n_tiles;
         l.n_tiles = (l.n_ftiles + gpu::kSuper - 1) / gpu::kSuper;
     }
-    const uint64_t warps = two ? gpu::kCWarps : dt.warps, bps = two ? dt.walk_blocks_per_sm : dt.blocks_per_sm;
+    const uint64_t warps = two ? gpu::kCWarps : (dt.dna ? dt.dna_warps : dt.warps);
+    const uint64_t bps = two ? dt.walk_blocks_per_sm : (dt.dna ? 1 : dt.blocks_per_sm);
     l.grid = std::min<uint64_t>(uint64_t(dt.sm_count) * bps, std::max<uint64_t>(1, (l.n_tiles + warps - 1) / warps));
     l.warps = l.grid * warps;
     return l;
@@ -843,6 +868,27 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         a.unit_next = ws.d_small + 6;
         // streamed chunks share the counter: zero it before each launch
         CK(cudaMemsetAsync(ws.d_small + 6, 0, sizeof(unsigned long long), ws.stream));
+    }
+    if (dt.dna) {
+        // pack pass (2-bit symbols + validity bits), then the direct-index scan
+        const uint64_t vw = (n_avail + 31) / 32 + 4;
+        ws.regrow(ws.d_packed, ws.packed_cap, 3 * vw);
+        const unsigned blocks = unsigned(std::min<uint64_t>((vw + 255) / 256, uint64_t(dt.sm_count) * 16));
+        gpu::pfac_pack_dna_kernel<<<std::max(1u, blocks), 256, 0, ws.stream>>>(d_text, n_avail, dt.view.symtab,
+                                                                               ws.d_packed, ws.d_packed + 2 * vw, vw);
+        CK(cudaGetLastError());
+        if (between) CK(cudaEventRecord(between, ws.stream));
+        a.packed = ws.d_packed;
+        a.valid = ws.d_packed + 2 * vw;
+        void* dparams[] = {&a};
+        const cudaError_t de = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.dna_kernel),
+                                                           dim3(unsigned(l.grid)), dim3(dt.dna_warps * 32), dparams,
+                                                           dt.dna_smem, ws.stream);
+        if (de != cudaSuccess) {
+            cudaGetLastError();
+            cuda_fail(de, "pfac_dna_kernel launch");
+        }
+        return 2;
     }
     void* params[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel(
@@ -1326,7 +1372,7 @@ LayoutInfo layout_info(const Trie& t)
     li.device_bytes = d->device_bytes;
     li.private_terminals = d->private_terminals;
     li.keyed_terminals = d->keyed_terminals;
-    li.filter_mode = d->kw == 0 ? 0u : d->filter_mode;
+    li.filter_mode = d->dna ? 5u : (d->kw == 0 ? 0u : (d->filter_mode == 5 ? 1u : d->filter_mode));
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
     return li;
 }
@@ -1442,7 +1488,7 @@ void session_run(Session* s, uint32_t iterations, int flush_l2, double* ms_each)
         CK(cudaEventRecord(s->evs[3 * i + 2], ws.stream));
     }
     s->last_iterations = iterations;
-    s->split = can_match && pipelined(dt, s->owned);
+    s->split = can_match && (pipelined(dt, s->owned) || dt.dna);
     s->complete = !can_match || fetch_small(ws, dt, s->owned); // grows buffers for the next run
     s->matches = can_match ? records_of(ws) : 0;
     for (uint32_t i = 0; i < iterations; ++i)
@@ -1453,7 +1499,7 @@ void session_split(Session* s, uint32_t n, double* first_ms, double* second_ms, 
 {
     DeviceGuard g(s->ws->device);
     if (kernels_per_scan)
-        *kernels_per_scan = pipelined(*s->dt, s->owned) ? (s->dt->sym_bits ? 3u : 2u) : 1u; // + pack pass
+        *kernels_per_scan = s->dt->dna ? 2u : (pipelined(*s->dt, s->owned) ? (s->dt->sym_bits ? 3u : 2u) : 1u);
     n = std::min(n, s->last_iterations);
     for (uint32_t i = 0; i < n; ++i) {
         const double total = elapsed_ms(s->evs[3 * i], s->evs[3 * i + 2]);

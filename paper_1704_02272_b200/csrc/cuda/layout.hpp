@@ -125,6 +125,31 @@ HFB_HD uint32_t jump_slot2(uint32_t key32, uint32_t bits)
     return filter2_hash(key32 * 0x9E3779B1u + 0x7F4A7C15u) >> (32 - bits);
 }
 
+// Direct-index form for alphabets of at most 4 symbols (filter mode 5: DNA).
+// Every pattern has kDnaK..kDnaMaxLen symbols.  The text is packed once per
+// scan to 2 bits per byte plus a validity bit per byte (pfac_pack_dna_kernel),
+// the first kDnaK symbols of a start are a 16-bit key, and one table blob --
+// small enough for shared memory -- answers everything a start needs:
+//   bitmap  u32[2048]     bit key: some pattern starts with these 8 symbols
+//                         (exact membership, no hashing)
+//   wrank   u16[2048]     set bits of the bitmap words before word w
+//   first   u16[keys+1]   key rank r -> its patterns [first[r], first[r+1])
+//   sym     u64[pats]     pattern symbols, 2 bits each, LSB first
+//   meta    u32[pats]     length << 16 | pattern id
+// Patterns are sorted by (key, length, id), so a start's records come out in
+// (length, id) order.  The blob is built only when the trie accepts exactly
+// its dictionary (image.cpp "path ids"): the records of a start are then
+// exactly the dictionary patterns that occur there, whatever the trie state.
+constexpr uint32_t kDnaK = 8;
+constexpr uint32_t kDnaMaxLen = 32;
+constexpr uint32_t kDnaMaxPerKey = 32;
+constexpr uint32_t kDnaWrankOff = 2048 * 4;          // byte offsets inside the blob
+constexpr uint32_t kDnaFirstOff = kDnaWrankOff + 2048 * 2;
+HFB_HD uint32_t dna_sym_off(uint32_t keys) { return (kDnaFirstOff + 2 * (keys + 1) + 7) & ~7u; }
+HFB_HD uint32_t dna_meta_off(uint32_t keys, uint32_t pats) { return dna_sym_off(keys) + 8 * pats; }
+HFB_HD uint32_t dna_blob_bytes(uint32_t keys, uint32_t pats) { return dna_meta_off(keys, pats) + 4 * pats; }
+constexpr uint32_t kDnaMaxBlob = 160 * 1024;
+
 // Device view of an uploaded image (plain pointers, passed by value).
 struct TrieView {
     const uint32_t* nodes;
@@ -158,6 +183,10 @@ struct TrieView {
     uint32_t jump_bits;      // 0 = no jump table (walks start at the root)
     const uint32_t* jump_ext; // per slot: first bucket entry + its next 16 pattern bytes, or null
     uint32_t min_emit;
+    const uint32_t* dna;      // direct-index form (filter mode 5): the table blob (layout above), or null
+    uint32_t dna_words;       // blob size in 32-bit words
+    uint32_t dna_keys;        // distinct kDnaK-symbol prefixes
+    uint32_t dna_pats;        // patterns
 };
 
 // First pattern byte an inline list entry stores (kJumpExtBytes from there):

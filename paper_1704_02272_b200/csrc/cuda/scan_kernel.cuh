@@ -104,6 +104,8 @@ struct ScanArgs {
     unsigned long long* unit_next; // dynamic unit counter (zero at launch)
     uint32_t* tile_region;      // staging region (warp) of each unit
     const uint32_t* packed;     // symbol-key mode: the text packed by pfac_pack_symbols_kernel, or null
+                                // (direct-index mode: by pfac_pack_dna_kernel)
+    const uint32_t* valid;      // direct-index mode: one bit per text byte, 1 = inside the alphabet
 };
 
 // ---- text and dictionary helpers --------------------------------------------------
@@ -767,6 +769,77 @@ struct Walker {
     }
 };
 
+// Phases 2 and 3 of every cooperative scan kernel (after phase 1 staged each
+// tile's records in its warp's region and wrote tile_count / tile_slot):
+//   grid sync -> phase 2: per-CTA sums of the tile counts over contiguous
+//     ranges of tiles;
+//   grid sync -> phase 3: each CTA scans its range and copies the staged
+//     records to their final offsets, so the output is in (start, length,
+//     id) order without a sort (the reference merges per-unit vectors and
+//     std::sorts, scan.cpp:104-111).
+// Tile i was staged by warp tile_region[i] (CANDS: dynamic units) or by
+// warp i % (grid * NW) (static interleave).
+template <uint32_t NW, bool CANDS>
+__device__ __forceinline__ void place_records(const ScanArgs& a, uint32_t* s_scr)
+{
+    constexpr uint32_t NT = NW * 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    // phase 2: per-CTA sums over contiguous chunks of tiles
+    cg::grid_group grid = cg::this_grid();
+    grid.sync();
+    const uint64_t nt = a.n_tiles, chunk = (nt + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = min(nt, uint64_t(blockIdx.x) * chunk), c1 = min(nt, c0 + chunk);
+    {
+        uint32_t s = 0;
+        for (uint64_t i = c0 + tid; i < c1; i += NT) s += a.tile_count[i];
+        uint32_t tot;
+        block_exclusive<NW>(s, s_scr, tot);
+        if (tid == 0) a.chunk_sum[blockIdx.x] = tot;
+    }
+    grid.sync();
+
+    // phase 3: scan the chunk, copy staged slices to their final offsets
+    // warp 0 sums the CTA sums (before this CTA, and all) for the whole CTA
+    __shared__ unsigned long long s_base[2];
+    if (warp == 0) {
+        unsigned long long before = 0, all = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            const unsigned long long v = a.chunk_sum[b];
+            before += b < blockIdx.x ? v : 0ull;
+            all += v;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            before += __shfl_xor_sync(0xFFFFFFFFu, before, d);
+            all += __shfl_xor_sync(0xFFFFFFFFu, all, d);
+        }
+        if (lane == 0) s_base[0] = before, s_base[1] = all;
+    }
+    __syncthreads();
+    const unsigned long long origin = *a.base_in;
+    unsigned long long base = origin + s_base[0];
+    const unsigned long long total = s_base[1];
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+        *a.total = total;
+        *a.base_out = origin + total;
+    }
+    const bool fits = origin + total <= a.out_cap && *a.warp_need == 0;
+    for (uint64_t r0 = c0; r0 < c1; r0 += NT) {
+        const uint64_t i = r0 + tid;
+        const uint32_t n = i < c1 ? a.tile_count[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_exclusive<NW>(n, s_scr, tot);
+        if (n && fits) {
+            const uint64_t region = CANDS ? a.tile_region[i] : i % (uint64_t(gridDim.x) * NW);
+            const uint4* src = reinterpret_cast<const uint4*>(a.stage + region * a.warp_cap) + a.tile_slot[i];
+            uint4* dst = reinterpret_cast<uint4*>(a.out) + base + ex;
+#pragma unroll 4
+            for (uint32_t k = 0; k < n; ++k) dst[k] = src[k];
+        }
+        base += tot;
+    }
+}
+
 // ---- PTX helpers: per-warp TMA bulk ring --------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
@@ -1061,60 +1134,7 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
     }
     if (lane == 0 && wk.cursor > a.warp_cap) atomicMax(a.warp_need, (unsigned long long)wk.cursor);
 
-    // phase 2: per-CTA sums over contiguous chunks of tiles
-    cg::grid_group grid = cg::this_grid();
-    grid.sync();
-    const uint64_t nt = a.n_tiles, chunk = (nt + gridDim.x - 1) / gridDim.x;
-    const uint64_t c0 = min(nt, uint64_t(blockIdx.x) * chunk), c1 = min(nt, c0 + chunk);
-    {
-        uint32_t s = 0;
-        for (uint64_t i = c0 + tid; i < c1; i += NT) s += a.tile_count[i];
-        uint32_t tot;
-        block_exclusive<NW>(s, s_scr, tot);
-        if (tid == 0) a.chunk_sum[blockIdx.x] = tot;
-    }
-    grid.sync();
-
-    // phase 3: scan the chunk, copy staged slices to their final offsets
-    // warp 0 sums the CTA sums (before this CTA, and all) for the whole CTA
-    __shared__ unsigned long long s_base[2];
-    if (warp == 0) {
-        unsigned long long before = 0, all = 0;
-        for (uint32_t b = lane; b < gridDim.x; b += 32) {
-            const unsigned long long v = a.chunk_sum[b];
-            before += b < blockIdx.x ? v : 0ull;
-            all += v;
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            before += __shfl_xor_sync(0xFFFFFFFFu, before, d);
-            all += __shfl_xor_sync(0xFFFFFFFFu, all, d);
-        }
-        if (lane == 0) s_base[0] = before, s_base[1] = all;
-    }
-    __syncthreads();
-    const unsigned long long origin = *a.base_in;
-    unsigned long long base = origin + s_base[0];
-    const unsigned long long total = s_base[1];
-    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
-        *a.total = total;
-        *a.base_out = origin + total;
-    }
-    const bool fits = origin + total <= a.out_cap && *a.warp_need == 0;
-    for (uint64_t r0 = c0; r0 < c1; r0 += NT) {
-        const uint64_t i = r0 + tid;
-        const uint32_t n = i < c1 ? a.tile_count[i] : 0u;
-        uint32_t tot;
-        const uint32_t ex = block_exclusive<NW>(n, s_scr, tot);
-        if (n && fits) {
-            const uint64_t region = CANDS ? a.tile_region[i] : i % (uint64_t(gridDim.x) * NW);
-            const uint4* src = reinterpret_cast<const uint4*>(a.stage + region * a.warp_cap) + a.tile_slot[i];
-            uint4* dst = reinterpret_cast<uint4*>(a.out) + base + ex;
-#pragma unroll 4
-            for (uint32_t k = 0; k < n; ++k) dst[k] = src[k];
-        }
-        base += tot;
-    }
+    place_records<NW, CANDS>(a, s_scr);
 }
 
 // Evicts the text from L2 between timed iterations when it would fit there.

@@ -20,6 +20,7 @@
 #include <array>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -30,7 +31,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + jump_ext.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + jump_ext.size() * 4 + dna.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -47,6 +48,7 @@ ImageOptions image_options_from_env()
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_JUMP_EXT")) o.jump_ext = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
+    if (const char* s = std::getenv("HEPFAC_DNA")) o.dna = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
         const std::string m = s;
         o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : (m == "l2" ? 4u : 0u));
@@ -738,6 +740,81 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             }
         }
     }
+    // ---- direct-index form (filter mode 5, layout.hpp) -------------------------
+    // Alphabets of at most 4 symbols whose every pattern has 8..32 symbols
+    // (c2: DNA, 10k patterns of 8-32): the byte-key path filters on 8-byte
+    // keys hashed into a bitmap and then, per surviving start, reads a jump
+    // slot and its inline list from L2 (two dependent round trips for the 14%
+    // of random DNA starts that are real 8-symbol prefixes).  Here the 16-bit
+    // key of 8 packed symbols indexes exact tables in shared memory and the
+    // start's patterns are compared 2 bits per symbol, with no L2 round trip.
+    if (opt.dna && im.filter_mode != 3 && im.dictionary_language && t.alphabet.size() <= 4 && P > 0 && P <= 65535) {
+        struct E {
+            uint32_t key, len, id;
+            uint64_t sym;
+        };
+        std::vector<E> es;
+        es.reserve(P);
+        bool ok = true;
+        for (size_t id = 0; id < P && ok; ++id) {
+            const auto& pat = t.patterns[id];
+            if (pat.size() < kDnaK || pat.size() > kDnaMaxLen) {
+                ok = false;
+                break;
+            }
+            uint64_t sym = 0;
+            for (size_t i = 0; i < pat.size(); ++i) {
+                const int s = t.alphabet.symbol_of(uint8_t(pat[i]));
+                if (s < 0) ok = false;
+                sym |= uint64_t(uint32_t(s) & 3u) << (2 * i);
+            }
+            es.push_back({uint32_t(sym & 0xFFFFu), uint32_t(pat.size()), uint32_t(id), sym});
+        }
+        if (ok) {
+            std::sort(es.begin(), es.end(), [](const E& x, const E& y) {
+                return x.key != y.key ? x.key < y.key : (x.len != y.len ? x.len < y.len : x.id < y.id);
+            });
+            std::vector<uint32_t> first;
+            std::vector<uint32_t> bitmap(2048, 0u);
+            for (size_t i = 0; i < es.size(); ++i) {
+                if (i == 0 || es[i].key != es[i - 1].key) {
+                    if (!first.empty() && i - first.back() > kDnaMaxPerKey) ok = false;
+                    first.push_back(uint32_t(i));
+                    bitmap[es[i].key >> 5] |= 1u << (es[i].key & 31u);
+                }
+            }
+            if (!first.empty() && es.size() - first.back() > kDnaMaxPerKey) ok = false;
+            const uint32_t nk = uint32_t(first.size());
+            first.push_back(uint32_t(es.size()));
+            const uint32_t bytes = dna_blob_bytes(nk, uint32_t(P));
+            if (ok && bytes <= kDnaMaxBlob) {
+                std::vector<uint8_t> blob(bytes, 0);
+                std::memcpy(blob.data(), bitmap.data(), 2048 * 4);
+                uint32_t run = 0;
+                for (uint32_t w = 0; w < 2048; ++w) {
+                    const uint16_t r = uint16_t(run);
+                    std::memcpy(blob.data() + kDnaWrankOff + 2 * w, &r, 2);
+                    run += uint32_t(__builtin_popcount(bitmap[w]));
+                }
+                for (uint32_t r = 0; r <= nk; ++r) {
+                    const uint16_t f = uint16_t(first[r]);
+                    std::memcpy(blob.data() + kDnaFirstOff + 2 * r, &f, 2);
+                }
+                for (size_t i = 0; i < es.size(); ++i) {
+                    std::memcpy(blob.data() + dna_sym_off(nk) + 8 * i, &es[i].sym, 8);
+                    const uint32_t meta = (es[i].len << 16) | es[i].id;
+                    std::memcpy(blob.data() + dna_meta_off(nk, uint32_t(P)) + 4 * i, &meta, 4);
+                }
+                im.dna.assign(bytes / 4, 0u);
+                std::memcpy(im.dna.data(), blob.data(), bytes);
+                im.dna_keys = nk;
+                im.dna_pats = uint32_t(P);
+                im.filter_mode = 5;
+                im.filter_pass = double(nk) / 65536.0;
+            }
+        }
+    }
+
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
     if (im.jump.empty()) im.jump.assign(kJumpWords, 0u), im.jump_ext.clear();

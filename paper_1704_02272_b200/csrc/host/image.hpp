@@ -30,7 +30,7 @@ struct GpuImage {
     std::vector<uint32_t> bk_span, bk_entry; // uint2 / uint4 records, see layout.hpp
 
     uint32_t filter_k = 0, filter_bits = 0, filter2_bits = 0;
-    uint32_t filter_mode = 0; // 0 none, 1 single probe, 2 pair probes (layout.hpp)
+    uint32_t filter_mode = 0; // 0 none, 1 single, 2 pair, 3 packed symbols, 4 single + L2, 5 direct index
     uint32_t sym_bits = 0;    // symbol-key mode: bits per packed symbol (filter_mode 3)
     uint32_t pair_shift = 0;
     double filter_pass = 1.0; // estimated fraction of random starts reaching the walk queue
@@ -41,6 +41,8 @@ struct GpuImage {
     std::vector<uint32_t> jump; // uint4 slots, see layout.hpp
     std::vector<uint32_t> jump_ext; // per slot: its inline pattern list (layout.hpp), or empty
     bool dictionary_language = false; // the trie accepts exactly its patterns (image.cpp "path ids")
+    std::vector<uint32_t> dna;        // direct-index form (filter_mode 5, layout.hpp), or empty
+    uint32_t dna_keys = 0, dna_pats = 0;
 
     uint32_t min_emit = UINT32_MAX; // shortest depth at which any start can report
     uint64_t reach = 0;             // max bytes one start may read; UINT64_MAX = unbounded
@@ -58,6 +60,7 @@ struct ImageOptions {
     bool jump_ext = true;           // inline pattern lists in the jump table (HEPFAC_JUMP_EXT=0 disables)
     uint32_t filter_mode = 0;       // 0 = cost model, 1 = single, 2 = pair (HEPFAC_FILTER_MODE)
     bool symbol_keys = true;        // packed-symbol filter keys for sigma <= 16 (HEPFAC_SYMBOL_KEYS=0 disables)
+    bool dna = true;                // direct-index form for sigma <= 4 (HEPFAC_DNA=0 disables)
 };
 
 ImageOptions image_options_from_env();

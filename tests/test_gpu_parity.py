@@ -577,3 +577,40 @@ def test_concurrent_scans_share_one_trie(gpu):
         th.join()
     assert not errors, errors
     assert all(results), results
+
+
+@pytest.mark.parametrize("alphabet", [b"ACGT", b"acgt", b"AC", b"XYZ"])
+@pytest.mark.parametrize("stages,depth", [(0, None), (1, 5), (2, None), (1, 9)])
+def test_direct_index_small_alphabet(gpu, monkeypatch, alphabet, stages, depth):
+    # Filter mode 5 (sigma <= 4, every pattern 8..32 symbols): exact
+    # shared-memory tables and 2-bit compares instead of trie walks.  Shared
+    # 8-symbol prefixes, nested patterns, bytes outside the alphabet inside
+    # occurrences, and patterns overhanging the text end; compared with the
+    # oracle and with the byte-key path (HEPFAC_DNA=0).
+    rng = np.random.default_rng(len(alphabet) * 7 + stages + (depth or 0))
+    a = gpu.alphabet(alphabet.decode())
+    syms = np.frombuffer(alphabet, dtype=np.uint8)
+    pats = set(pattern_set(rng, syms, 600, 8, 32))
+    base = bytes(syms[rng.integers(0, syms.size, size=32)])
+    pats |= {base[:n] for n in (8, 9, 12, 20, 32)}  # nested, one 8-symbol prefix
+    pats = sorted(pats)
+    t = gpu.build_trie(gpu.patterns(pats, a))
+    if stages:
+        t, _ = t.compress(stages)
+    if depth:
+        t, _ = t.truncate(depth)
+    assert gpu.layout_info(t)["filter_mode"] == 5
+    tx = text(rng, syms, (1 << 20) + 4097)
+    for i in range(0, tx.size - 40, 613):
+        plant(tx, pats[i % len(pats)], i)
+    for i in range(3000, tx.size - 40, 50021):
+        plant(tx, base, i)
+        tx[i + 10] = ord("N")  # kills the 12-, 20- and 32-symbol occurrences
+    plant(tx, base, tx.size - 20)  # 8, 9, 12 fit; 20 and 32 overhang the end
+    want = oracle.naive_find_all(tx, pats)
+    got = gpu.scan(t, tx)
+    assert same(got, want)
+    monkeypatch.setenv("HEPFAC_DNA", "0")
+    t2 = gpu.build_trie(gpu.patterns(pats, a))
+    assert gpu.layout_info(t2)["filter_mode"] != 5
+    assert same(gpu.scan(t2, tx), want)
