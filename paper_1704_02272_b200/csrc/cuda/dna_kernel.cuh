@@ -32,10 +32,32 @@ namespace hfb::gpu {
 constexpr uint32_t kDnaQueue = 1024;      // per-warp queue of tile offsets (>= 2 chunks)
 constexpr uint32_t kDnaChunk = 512;       // starts per warp chunk (16 per lane)
 
+// One 32-byte block through the symbol table: 32 codes (two words) and 32
+// validity bits; bytes at or past `n` are invalid.
+__device__ __forceinline__ void pack_block_table(const uint32_t (&bytes)[8], uint64_t b0, uint64_t n,
+                                                 const uint32_t* tab, uint32_t& lo, uint32_t& hi, uint32_t& ok)
+{
+    lo = hi = ok = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < 32; ++i) {
+        const uint32_t c = b0 + i < n ? tab[(bytes[i / 4] >> (8 * (i % 4))) & 0xFFu] : 0u;
+        ok |= (c >> 2) << i;
+        if (i < 16) lo |= (c & 3u) << (2 * i);
+        else hi |= (c & 3u) << (2 * (i - 16));
+    }
+}
+
 // Packs text[0, n) into 2-bit symbols and validity bits; words past the text
 // (the kernel reads up to 3 packed / 2 validity words ahead) are zero.
+// FORMULA: the alphabet's symbol of byte b is ((b >> 1) ^ (b >> 2)) & 3
+// (true of "ACGT" and "acgt"; the host checks): four codes per word come from
+// three instructions, and a word is valid when every byte equals the
+// alphabet byte of its code (one PRMT against the packed alphabet `symw`).
+// Words with a byte outside the alphabet (rare) and the last, partial block
+// take the table path.
+template <bool FORMULA>
 __global__ void __launch_bounds__(256) pfac_pack_dna_kernel(const uint8_t* __restrict__ text, uint64_t n,
-                                                           const uint16_t* __restrict__ symtab,
+                                                           const uint16_t* __restrict__ symtab, uint32_t symw,
                                                            uint32_t* __restrict__ packed,
                                                            uint32_t* __restrict__ valid, uint64_t vwords)
 {
@@ -55,13 +77,24 @@ __global__ void __launch_bounds__(256) pfac_pack_dna_kernel(const uint8_t* __res
             bytes[4] = y.x, bytes[5] = y.y, bytes[6] = y.z, bytes[7] = y.w;
         }
         uint32_t lo = 0, hi = 0, ok = 0;
+        bool table = !FORMULA || b0 + 32 > n;
+        if (!table) {
+            bool clean = true;
 #pragma unroll
-        for (uint32_t i = 0; i < 32; ++i) {
-            const uint32_t c = b0 + i < n ? tab[(bytes[i / 4] >> (8 * (i % 4))) & 0xFFu] : 0u;
-            ok |= (c >> 2) << i;
-            if (i < 16) lo |= (c & 3u) << (2 * i);
-            else hi |= (c & 3u) << (2 * (i - 16));
+            for (uint32_t q = 0; q < 8; ++q) {
+                const uint32_t c = ((bytes[q] >> 1) ^ (bytes[q] >> 2)) & 0x03030303u;
+                const uint32_t t = c | (c >> 4);                        // codes of bytes 0,1 / 2,3 in nibbles
+                const uint32_t canon = __byte_perm(symw, 0u, __byte_perm(t, 0u, 0x0020u));
+                clean = clean && canon == bytes[q];
+                const uint32_t u = c | (c >> 6);                        // 4 codes -> bits 0-3, 16-19
+                const uint32_t p8 = (u & 0xFu) | ((u >> 12) & 0xF0u);
+                if (q < 4) lo |= p8 << (8 * q);
+                else hi |= p8 << (8 * (q - 4));
+            }
+            ok = 0xFFFFFFFFu;
+            table = !clean;
         }
+        if (table) pack_block_table(bytes, b0, n, tab, lo, hi, ok);
         packed[2 * w] = lo;
         packed[2 * w + 1] = hi;
         valid[w] = ok;
@@ -110,25 +143,38 @@ __global__ void __launch_bounds__(NW * 32, 1) pfac_dna_kernel(const __grid_const
                 const uint32_t sh = 2u * uint32_t(s & 15u);
                 const uint32_t x0 = __ldg(P + wi), x1 = __ldg(P + wi + 1), x2 = __ldg(P + wi + 2);
                 const uint64_t vi = s >> 5;
-                const uint32_t vv = __funnelshift_r(__ldg(V + vi), __ldg(V + vi + 1), uint32_t(s & 31u));
-                const uint64_t txt = (uint64_t(__funnelshift_r(x1, x2, sh)) << 32) | __funnelshift_r(x0, x1, sh);
-                const uint32_t key = uint32_t(txt) & 0xFFFFu;
+                // ~validity of bytes [s, s + 32): 0 bits = inside the alphabet
+                // and the text (the pack pass leaves bytes past the end invalid)
+                const uint32_t nv = ~__funnelshift_r(__ldg(V + vi), __ldg(V + vi + 1), uint32_t(s & 31u));
+                const uint32_t tlo = __funnelshift_r(x0, x1, sh), thi = __funnelshift_r(x1, x2, sh);
+                const uint32_t key = tlo & 0xFFFFu;
                 const uint32_t word = s_bits[key >> 5];
-                const uint32_t r = s_wrank[key >> 5] + __popc(word & ((1u << (key & 31u)) - 1u));
+                const uint32_t r = s_wrank[key >> 5] + __popc(word & __funnelshift_lc(~0u, 0u, key & 31u));
                 f0 = s_first[r];
                 const uint32_t cnt = s_first[r + 1] - f0;
-                const uint64_t room = a.n_avail - s;
-                for (uint32_t k = 0; k < cnt; ++k) {
-                    const uint64_t sym = s_sym[f0 + k];
+                // pattern k matches: its 2-bit symbols equal the text's and
+                // its len bytes are valid (len in [8, 32])
+                auto test = [&](uint32_t k) -> uint32_t {
+                    const uint2 sym = *reinterpret_cast<const uint2*>(s_sym + f0 + k);
                     const uint32_t len = s_meta[f0 + k] >> 16;
-                    const uint64_t lm = len >= 32 ? ~0ull : (1ull << (2 * len)) - 1ull;
-                    const uint32_t vm = len >= 32 ? ~0u : (1u << len) - 1u;
-                    if (((txt ^ sym) & lm) == 0 && (vv & vm) == vm && len <= room) mask |= 1u << k;
-                }
+                    const uint32_t mlo = __funnelshift_lc(~0u, 0u, 2 * len);
+                    const uint32_t mhi = __funnelshift_lc(~0u, 0u, max(2 * len, 32u) - 32u);
+                    const uint32_t diff = ((tlo ^ sym.x) & mlo) | ((thi ^ sym.y) & mhi) | (nv << (32u - len));
+                    return diff == 0 ? 1u : 0u;
+                };
+                mask = test(0); // every candidate has at least one pattern
+                for (uint32_t k = 1; k < cnt; ++k) mask |= test(k) << k;
             }
+            uint64_t at = cursor;
             uint32_t tot;
-            const uint32_t ex = warp_exclusive(__popc(mask), lane, tot);
-            uint64_t at = cursor + ex;
+            const uint32_t nm = __popc(mask);
+            if (!__any_sync(0xFFFFFFFFu, nm > 1)) { // common: at most one record per start
+                const uint32_t b = __ballot_sync(0xFFFFFFFFu, nm != 0);
+                at += __popc(b & ((1u << lane) - 1u));
+                tot = __popc(b);
+            } else {
+                at += warp_exclusive(nm, lane, tot);
+            }
             for (uint32_t m = mask; m; m &= m - 1, ++at) {
                 const uint32_t meta = s_meta[f0 + __ffs(m) - 1];
                 const uint64_t g = a.g0 + s;
@@ -153,13 +199,14 @@ __global__ void __launch_bounds__(NW * 32, 1) pfac_dna_kernel(const __grid_const
             uint32_t v = __funnelshift_r(__ldg(V + vi), __ldg(V + vi + 1), 16u * uint32_t(wi & 1u));
             v &= v >> 1, v &= v >> 2, v &= v >> 4; // bit j: bytes j..j+7 are in the alphabet
             const int32_t r = int32_t(rem) - int32_t(c * kDnaChunk + 16u * lane);
-            uint32_t m = 0;
+            uint32_t m = 0; // start j's bit enters at 31 and ends at 16 + j
 #pragma unroll
             for (uint32_t j = 0; j < 16; ++j) {
-                const uint32_t key = (j ? __funnelshift_r(p0, p1, 2 * j) : p0) & 0xFFFFu;
-                m |= ((s_bits[key >> 5] >> (key & 31u)) & 1u) << j;
+                const uint32_t win = j ? __funnelshift_r(p0, p1, 2 * j) : p0; // key = low 16 bits
+                const uint32_t word = s_bits[(win >> 5) & 0x7FFu];
+                m = __funnelshift_r(m, __funnelshift_r(word, 0u, win), 1); // bit (key & 31) of word
             }
-            m &= v & (r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u));
+            m = (m >> 16) & v & (r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u));
             if (!__any_sync(0xFFFFFFFFu, m)) continue;
             uint32_t tot;
             const uint32_t ex = warp_exclusive(__popc(m), lane, tot);

@@ -416,6 +416,18 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
         v.dna_words = uint32_t(im.dna.size());
         v.dna_keys = im.dna_keys;
         v.dna_pats = im.dna_pats;
+        // the pack pass's arithmetic form, when the alphabet follows it
+        uint32_t symw = 0;
+        bool formula = im.symtab.size() == 256;
+        uint32_t count = 0;
+        for (uint32_t b = 0; b < 256 && formula; ++b) {
+            const uint16_t sy = im.symtab[b];
+            if (sy == kNoSym) continue;
+            ++count;
+            if (sy > 3 || (((b >> 1) ^ (b >> 2)) & 3u) != sy) formula = false;
+            else symw |= b << (8 * sy);
+        }
+        v.dna_symw = formula && count == 4 ? symw : 0u;
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
         // 32 warps when the tables and 32 queues fit next to the static
@@ -874,8 +886,12 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         const uint64_t vw = (n_avail + 31) / 32 + 4;
         ws.regrow(ws.d_packed, ws.packed_cap, 3 * vw);
         const unsigned blocks = unsigned(std::min<uint64_t>((vw + 255) / 256, uint64_t(dt.sm_count) * 16));
-        gpu::pfac_pack_dna_kernel<<<std::max(1u, blocks), 256, 0, ws.stream>>>(d_text, n_avail, dt.view.symtab,
-                                                                               ws.d_packed, ws.d_packed + 2 * vw, vw);
+        if (dt.view.dna_symw)
+            gpu::pfac_pack_dna_kernel<true><<<std::max(1u, blocks), 256, 0, ws.stream>>>(
+                d_text, n_avail, dt.view.symtab, dt.view.dna_symw, ws.d_packed, ws.d_packed + 2 * vw, vw);
+        else
+            gpu::pfac_pack_dna_kernel<false><<<std::max(1u, blocks), 256, 0, ws.stream>>>(
+                d_text, n_avail, dt.view.symtab, 0u, ws.d_packed, ws.d_packed + 2 * vw, vw);
         CK(cudaGetLastError());
         if (between) CK(cudaEventRecord(between, ws.stream));
         a.packed = ws.d_packed;

@@ -187,6 +187,8 @@ struct TrieView {
     uint32_t dna_words;       // blob size in 32-bit words
     uint32_t dna_keys;        // distinct kDnaK-symbol prefixes
     uint32_t dna_pats;        // patterns
+    uint32_t dna_symw;        // the alphabet bytes, symbol i in byte i, when symbols follow the
+                              // formula ((b >> 1) ^ (b >> 2)) & 3 ("ACGT", "acgt"); else 0
 };
 
 // First pattern byte an inline list entry stores (kJumpExtBytes from there):
