@@ -411,6 +411,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
     v.jump_bits = im.jump_bits;
     v.jump_ext = im.jump_ext.empty() ? nullptr : d->upload(im.jump_ext);
     v.min_emit = im.min_emit;
+    v.filter_l1 = im.filter_l1.empty() ? nullptr : d->upload(im.filter_l1);
+    v.filter_l1_words = uint32_t(im.filter_l1.size());
     if (im.filter_mode == 5) {
         v.dna = d->upload(im.dna);
         v.dna_words = uint32_t(im.dna.size());
@@ -473,10 +475,13 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->walk_blocks_per_sm, d->walk_kernel,
                                                          int(gpu::kCWarps * 32), d->walk_smem));
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
-        d->filter_smem = size_t(v.filter_words) * 4 +
-                         ((im.filter_mode == 3 || im.filter_mode == 4)
-                              ? 0
-                              : (pair_queue_form() ? gpu::filter_smem_fixed_bytes() : gpu::filter2_smem_fixed_bytes()));
+        if (im.filter_mode == 4) // the whole shared-memory level, nothing else
+            d->filter_smem = size_t(v.filter_l1_words) * 4;
+        else
+            d->filter_smem = size_t(v.filter_words) * 4 +
+                             (im.filter_mode == 3 ? 0
+                                                  : (pair_queue_form() ? gpu::filter_smem_fixed_bytes()
+                                                                       : gpu::filter2_smem_fixed_bytes()));
         allow_max_smem(d->filter_fn, device);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
                                                          d->filter_smem));
@@ -836,8 +841,8 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         if (ws.cand_cap == 0) ws.ensure_cand(fwarps, n_own / 256 / fwarps + 256);
         ws.ensure_cand(fwarps, ws.cand_cap);
         gpu::FilterArgs f{};
-        f.table = dt.view.filter;
-        f.table_words = dt.view.filter_words;
+        f.table = dt.filter_mode == 4 ? dt.view.filter_l1 : dt.view.filter;
+        f.table_words = dt.filter_mode == 4 ? dt.view.filter_l1_words : dt.view.filter_words;
         f.pair_shift = dt.view.pair_shift;
         f.text = d_text;
         f.n_avail = n_avail;

@@ -476,6 +476,19 @@ __device__ __forceinline__ uint32_t f_key(const uint32_t (&w)[6], int j, uint32_
     return lo + hi * 0x85EBCA77u; // filter_fold
 }
 
+// L2 bitmap word: random 4-byte reads with no reuse in L1 (HFB_PROBE_NA=1:
+// not allocated in L1).
+__device__ __forceinline__ uint32_t probe_l2(const uint32_t* p)
+{
+#if defined(HFB_PROBE_NA) && HFB_PROBE_NA
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 template <int KW>
 __global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __grid_constant__ FilterArgs a)
 {
@@ -484,8 +497,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __gr
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
     for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
     __syncthreads();
-    const uint8_t* tbytes = fsmem;
-    const uint32_t mask4 = (a.table_words - 1u) << 2;
+    const uint32_t words = a.table_words; // filter_l1_word range (any count)
     const uint32_t k = a.filter_k;
     const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
     const uint32_t* l2 = a.table2;
@@ -536,10 +548,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __gr
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const uint32_t key = f_key<KW>(w, j, mhi);
-                const uint32_t word = *reinterpret_cast<const uint32_t*>(tbytes + (__umulhi(key, kFilterMul) & mask4));
+                const uint32_t word = s_tab[__umulhi(key * kFilterMul, words)]; // filter_l1_word
                 const bool hit = ((valid >> j) & 1u) && int32_t(word << (key & 31u)) < 0;
                 const uint32_t s2 = filter2_hash(key) >> sh2;
-                w2[j] = hit ? __ldg(l2 + (s2 >> 5)) >> (s2 & 31u) : 0u;
+                w2[j] = hit ? probe_l2(l2 + (s2 >> 5)) >> (s2 & 31u) : 0u;
             }
 #pragma unroll
             for (int j = 0; j < 16; ++j) m |= (w2[j] & 1u) << j;

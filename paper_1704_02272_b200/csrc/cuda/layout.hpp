@@ -63,6 +63,20 @@ HFB_HD uint32_t filter_word(uint32_t key32, uint32_t word_bits)
     return uint32_t((uint64_t(key32) * kFilterMul) >> 34) & ((1u << word_bits) - 1u);
 }
 HFB_HD uint32_t filter_mask_bit(uint32_t key32) { return 0x80000000u >> (key32 & 31u); }
+// Filter mode 4's shared-memory level is as large as the L1 data cache
+// allows, so its word count is not a power of two: multiply-high range
+// reduction.  192 KiB (1.57 M bits) measured best at c5 1M patterns (463
+// GB/s, against 384 at 128 KiB): 200 KiB or more moves the shared-memory
+// carveout to 228 KiB, and the 28 KiB left to L1 starves the filter pass's
+// 16-byte text loads and L2 probes (273-292 GB/s).
+#ifndef HFB_L1_KIB
+#define HFB_L1_KIB 192
+#endif
+constexpr uint32_t kL1Words = HFB_L1_KIB * 1024 / 4;
+HFB_HD uint32_t filter_l1_word(uint32_t key32, uint32_t words)
+{
+    return uint32_t((uint64_t(key32 * kFilterMul) * words) >> 32);
+}
 
 // Start filter, pair form (k >= 4).  One 32-bit word per 3-byte "middle"
 // M = (b1, b2, b3) serves two starts: the start at M's first byte (its 4th
@@ -183,6 +197,8 @@ struct TrieView {
     uint32_t jump_bits;      // 0 = no jump table (walks start at the root)
     const uint32_t* jump_ext; // per slot: first bucket entry + its next 16 pattern bytes, or null
     uint32_t min_emit;
+    const uint32_t* filter_l1; // single + L2 form (filter mode 4): the shared-memory level, filter_l1_words
+    uint32_t filter_l1_words;  // words (any count: word = umulhi(key * kFilterMul, words), bit key & 31)
     const uint32_t* dna;      // direct-index form (filter mode 5): the table blob (layout above), or null
     uint32_t dna_words;       // blob size in 32-bit words
     uint32_t dna_keys;        // distinct kDnaK-symbol prefixes

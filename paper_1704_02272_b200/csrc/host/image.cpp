@@ -31,7 +31,7 @@ size_t GpuImage::device_bytes() const
 {
     return nodes.size() * 4 + term_id.size() * 4 + bucket_of.size() * 4 + pat_bytes.size() +
            pat_off.size() * 8 + pat_len.size() * 4 + ht_key.size() * 8 + ht_id.size() * 4 +
-           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + jump_ext.size() * 4 + dna.size() * 4 + 512;
+           bk_span.size() * 4 + bk_entry.size() * 4 + path_id.size() * 4 + filter.size() * 4 + filter2.size() * 4 + key4.size() * 4 + jump.size() * 4 + jump_ext.size() * 4 + dna.size() * 4 + filter_l1.size() * 4 + 512;
 }
 
 ImageOptions image_options_from_env()
@@ -635,7 +635,16 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             if (im.filter_mode == 1 && k >= 4 && im.filter2_bits &&
                 (opt.filter_mode == 4 || (opt.filter_mode == 0 && p_single > 0.25))) {
                 im.filter_mode = 4;
-                im.filter_pass = p_single * double(popcount(im.filter2)) / double(uint64_t(1) << im.filter2_bits);
+                // its shared-memory level: 192 KiB (1.57 M bits, layout.hpp;
+                // c5 1M: 47% of random starts pass instead of 61% with 2^20
+                // bits), so fewer starts probe L2
+                im.filter_l1.assign(kL1Words, 0u);
+                for (uint64_t g : grams) {
+                    const uint32_t k32 = filter_fold(g);
+                    im.filter_l1[filter_l1_word(k32, kL1Words)] |= filter_mask_bit(k32);
+                }
+                const double f_l1 = double(popcount(im.filter_l1)) / double(uint64_t(32) * kL1Words);
+                im.filter_pass = f_l1 * double(popcount(im.filter2)) / double(uint64_t(1) << im.filter2_bits);
             }
             if (opt.jump) {
                 std::vector<JumpEntry> entries(grams.size());

@@ -36,6 +36,7 @@ struct GpuImage {
     double filter_pass = 1.0; // estimated fraction of random starts reaching the walk queue
     uint64_t filter_paths = 0;
     std::vector<uint32_t> filter, filter2;
+    std::vector<uint32_t> filter_l1; // filter mode 4: the shared-memory level (kL1Words words)
     std::vector<uint32_t> key4; // pair pipeline: single-probe bitmap over 4-byte path prefixes
     uint32_t jump_bits = 0;     // log2 slots of the depth-k jump table, 0 = none
     std::vector<uint32_t> jump; // uint4 slots, see layout.hpp
