@@ -313,11 +313,12 @@ bool pair_pipeline_enabled()
     return !s || std::strtol(s, nullptr, 10) != 0;
 }
 
-// HEPFAC_PAIR_QUEUE=0: the in-lane form of the pair filter pass (A/B only).
+// HEPFAC_PAIR_QUEUE=1: the queue form of the pair filter pass (A/B only; the
+// in-lane form measured 0.5-8% faster: c3, c4 sigma=256, c5 10k).
 bool pair_queue_form()
 {
     const char* s = std::getenv("HEPFAC_PAIR_QUEUE");
-    return !s || std::strtol(s, nullptr, 10) != 0;
+    return s && std::strtol(s, nullptr, 10) != 0;
 }
 
 // Launches covering fewer starts than this use the one-pass kernel: the

@@ -324,17 +324,25 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const _
             uint4 cur[kFChunks];
 #pragma unroll
             for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
-            if (s + 1 < steps) {
-                const uint64_t nb = sbase + kFStep;
-                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
-                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
+            // the next step's loads: issued after this step's second level, so
+            // their registers are not live across it (+2% at c3 against issuing
+            // them here; HFB_LATE_PREFETCH=0 restores that)
+            auto prefetch = [&]() {
+                if (s + 1 < steps) {
+                    const uint64_t nb = sbase + kFStep;
+                    if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
+                        const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
 #pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
-                } else {
+                        for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
+                    } else {
 #pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
+                        for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
+                    }
                 }
-            }
+            };
+#if defined(HFB_LATE_PREFETCH) && !HFB_LATE_PREFETCH
+            prefetch();
+#endif
             // the word after the step (lane 0 of the next step's first chunk)
             uint32_t tail = 0;
             if (lane == 31 && sbase + kFStep < avail16)
@@ -363,35 +371,57 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const _
                 else if (b == 2) m23 = m;
                 else m23 |= m << 16;
             }
-            if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
+            if (!__any_sync(0xFFFFFFFFu, m01 | m23)) {
+#if !defined(HFB_LATE_PREFETCH) || HFB_LATE_PREFETCH
+                prefetch();
+#endif
+                continue;
+            }
 
             // second level, in-lane: the other role of each first-level
-            // survivor, highest bit first (x: chunks 0-1, y: chunks 2-3; bit j
-            // = chunk j/16, position j%16 of the lane's slice).  One loop over
-            // both words: a step costs max over lanes of the lane's survivors.
-            // Failing bits are cleared from m01 / m23.
+            // survivor, highest bit first (bit j of a word = chunk j/16,
+            // position j%16 of the lane's slice; m01: chunks 0-1, m23: 2-3).
+            // One loop over both words -- a step costs max over lanes of the
+            // lane's survivors -- walking m01 first, then m23: the switch is a
+            // rare branch instead of a select on every variable.  Failing bits
+            // are cleared.
             {
-                uint32_t x = m01, y = m23;
-                const uint32_t base = 16u * lane;
-                while (x | y) {
-                    const bool first = x != 0;
-                    const uint32_t j = 31u - __clz(first ? x : y);
-                    const uint32_t bit = 1u << j;
-                    if (first) x ^= bit;
-                    else y ^= bit;
-                    // staging offset: chunk * 512 + 16 * lane + position
-                    const uint32_t so = (first ? base : base + 2u * kFChunk) + j + (j >> 4) * (kFChunk - 16u);
-                    const uint32_t t = staged4(so);             // bytes p0 p1 p2 p3 of the start
-                    const bool odd = j & 1u;                    // odd starts passed role B: test A
-                    const uint32_t mid = odd ? (t >> 8) : t;    // A: H(p1 p2 p3); B: H(p0 p1 p2)
-                    const uint32_t amt = odd ? t : (t >> 24);   // A: bit p0;       B: bit p3
-                    const uint32_t word = s_tab[(mid * kPairMul) >> shift];
-                    if (int32_t(word << (amt & 31u)) >= 0) {
-                        if (first) m01 ^= bit;
-                        else m23 ^= bit;
+                // loop constants kept opaque, so they stay in registers
+                uint32_t k_one, k_mul, k_shift;
+                asm("mov.u32 %0, 1;" : "=r"(k_one));
+                asm("mov.u32 %0, %1;" : "=r"(k_mul) : "n"(kPairMul));
+                asm("mov.u32 %0, %1;" : "=r"(k_shift) : "r"(shift));
+                uint32_t fail01 = 0, fail23 = 0;
+#pragma unroll
+                for (uint32_t half = 0; half < 2; ++half) {
+                    const uint32_t base = stage_s + 16u * lane + half * 2u * kFChunk;
+                    uint32_t fail = 0;
+                    for (uint32_t x = half ? m23 : m01; x;) {
+                        uint32_t j;
+                        asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(x)); // highest set bit
+                        const uint32_t bit = k_one << j;
+                        x ^= bit;
+                        const uint32_t at = base + j + (j >> 4) * (kFChunk - 16u); // + chunk * 512 + position
+                        uint32_t w0, w1, t;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(at & ~3u));
+                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w1) : "r"(at & ~3u));
+                        asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(t) : "r"(w0), "r"(w1), "r"(at)); // p0 p1 p2 p3
+                        // odd starts passed role B and test A: H(p1 p2 p3), bit p0;
+                        // even ones test B: H(p0 p1 p2), bit p3
+                        const bool odd = j & 1u;
+                        const uint32_t mid = odd ? t >> 8 : t, amt = odd ? t : t >> 24;
+                        const uint32_t word = f_lds(tbase + (((mid * k_mul) >> k_shift) << 2));
+                        if (int32_t(__funnelshift_l(0u, word, amt)) >= 0) fail |= bit;
                     }
+                    if (half) fail23 = fail;
+                    else fail01 = fail;
                 }
+                m01 &= ~fail01;
+                m23 &= ~fail23;
             }
+#if !defined(HFB_LATE_PREFETCH) || HFB_LATE_PREFETCH
+            prefetch();
+#endif
             if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
             // final survivors in start order (chunk, lane, position): one warp
             // scan of the lane's four per-chunk counts packed in 8-bit fields

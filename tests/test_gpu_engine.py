@@ -166,7 +166,7 @@ def test_output_invariant_across_engine_configurations(gpu, monkeypatch):
     pats, tx = dense_instance(21, mib=3, every=509)
     t = build(gpu, pats, 256, 1, 5)
     want = oracle.naive_find_all(tx, pats)
-    combos = [{}, {"HEPFAC_PIPELINE_MIN_MIB": "0"}, {"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_QUEUE": "0"},
+    combos = [{}, {"HEPFAC_PIPELINE_MIN_MIB": "0"}, {"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_QUEUE": "1"},
               {"HEPFAC_CHUNK_MIB": "1"}, {"HEPFAC_CHUNK_MIB": "1", "HEPFAC_PIPELINE_MIN_MIB": "0"},
               {"HEPFAC_DEVICES": "0,0,0"}, {"HEPFAC_DEVICES": "0,0", "HEPFAC_PIPELINE_MIN_MIB": "0"}]
     keys = {k for c in combos for k in c}
