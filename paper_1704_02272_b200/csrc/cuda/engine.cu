@@ -468,7 +468,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
             if (im.filter_mode == 4)
                 d->filter_fn = d->kw == 3 ? gpu::pfac_l2_filter_kernel<3> : gpu::pfac_l2_filter_kernel<2>;
             else
-                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_kernel : gpu::pfac_pair_filter2_kernel;
+                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_queue_kernel : gpu::pfac_pair_filter_kernel;
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues

@@ -91,7 +91,7 @@ __device__ __forceinline__ uint32_t f_pair_level1(const uint32_t (&w)[5], uint32
     return __brev((m0 << 24) | (m1 << 16)); // start j at bit j
 }
 
-__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __grid_constant__ FilterArgs a)
+__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_queue_kernel(const __grid_constant__ FilterArgs a)
 {
     extern __shared__ __align__(128) uint8_t fsmem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -276,7 +276,7 @@ __device__ __forceinline__ uint32_t f_pair_probe(const uint32_t* __restrict__ ta
     return tab[(mid * kPairMul) >> shift];
 }
 
-__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter2_kernel(const __grid_constant__ FilterArgs a)
+__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __grid_constant__ FilterArgs a)
 {
     extern __shared__ __align__(128) uint8_t fsmem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;

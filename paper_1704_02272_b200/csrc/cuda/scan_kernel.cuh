@@ -202,30 +202,36 @@ __device__ __noinline__ uint32_t resolve_slice(const ScanArgs& a, uint64_t start
     }
 }
 
-// Records of one walk round: the first kRegRecords stay in registers;
-// a re-walk in write mode (dst != nullptr) emits the rest.
+// Records of one walk round.  Every record of a walk has the walk's start,
+// so the first kRegRecords keep only (length, id) in registers (Sink); a
+// re-walk emits the rest straight to the staging region (WriteSink).  Two
+// types, so the walk carries only the state its mode needs.
+// (Keeping these records in shared-memory slots instead, to lower register
+// pressure, measured 2-15% slower: c3, c4 sigma=4, c5 100k.)
 struct Sink {
     uint32_t n = 0;
-    uint4 r0, r1;
-    hepfac_match_t* dst = nullptr;
-    uint64_t at = 0, cap = 0;
-    uint32_t skip = 0;
+    uint32_t l0 = 0, i0 = 0, l1 = 0, i1 = 0;
+
+    __device__ __forceinline__ void put(uint64_t, uint32_t l, uint32_t i)
+    {
+        if (n == 0) l0 = l, i0 = i;
+        else if (n == 1) l1 = l, i1 = i;
+        ++n;
+    }
+};
+struct WriteSink {
+    hepfac_match_t* dst;
+    uint64_t at, cap;
+    uint32_t skip;
 
     __device__ __forceinline__ void put(uint64_t s, uint32_t l, uint32_t i)
     {
-        const uint4 v = make_uint4(uint32_t(s), uint32_t(s >> 32), l, i);
-        if (dst) {
-            if (skip) {
-                --skip;
-            } else {
-                if (at < cap) reinterpret_cast<uint4*>(dst)[at] = v;
-                ++at;
-            }
+        if (skip) {
+            --skip;
             return;
         }
-        if (n == 0) r0 = v;
-        else if (n == 1) r1 = v;
-        ++n;
+        if (at < cap) reinterpret_cast<uint4*>(dst)[at] = make_uint4(uint32_t(s), uint32_t(s >> 32), l, i);
+        ++at;
     }
 };
 
@@ -256,7 +262,8 @@ __device__ __forceinline__ bool same_at(const ScanArgs& a, uint64_t start, uint6
 // Depth-limit verification (scan.cpp:37-49): bucket entries are pre-sorted by
 // (length, id), which is the order the records must appear in.  One load
 // gives the bucket's span, one load per entry its id, length and bytes.
-__device__ __forceinline__ void verify_span(const ScanArgs& a, uint2 span, uint64_t start, Sink& sink)
+template <class S>
+__device__ __forceinline__ void verify_span(const ScanArgs& a, uint2 span, uint64_t start, S& sink)
 {
     const TrieView& t = a.trie;
     // Every bucket pattern spells the node's depth-limit path (the walk just
@@ -271,7 +278,8 @@ __device__ __forceinline__ void verify_span(const ScanArgs& a, uint2 span, uint6
     }
 }
 
-__device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, Sink& sink)
+template <class S>
+__device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, uint64_t start, S& sink)
 {
     const TrieView& t = a.trie;
     verify_span(a, __ldg(reinterpret_cast<const uint2*>(t.bk_span) + __ldg(t.bucket_of + node)), start, sink);
@@ -285,9 +293,9 @@ __device__ __forceinline__ void verify_bucket(const ScanArgs& a, uint32_t node, 
 //
 // A walk may begin below the root: (node, depth) from the jump table, which
 // is only used for depth <= min_emit, where nothing above can report.
-template <bool GROUPED, bool IDENT, bool PAR>
+template <bool GROUPED, bool IDENT, bool PAR, class S>
 __device__ __forceinline__ void walk(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
-                                     uint32_t node, uint32_t depth, Sink& sink, uint32_t pend = kNoId)
+                                     uint32_t node, uint32_t depth, S& sink, uint32_t pend = kNoId)
 {
     const TrieView& t = a.trie;
     const uint32_t room = uint32_t(min(a.n_avail - start, uint64_t(0x7FFFFFFF)));
@@ -580,9 +588,9 @@ __device__ __forceinline__ JumpHit jump_lookup(const TrieView& t, uint64_t win)
 // A walk that starts at the depth limit (k == limit): the node's terminal
 // record and its bucket come from the jump slot (walk() semantics at the
 // limit: terminal first, then the bucket in (length, id) order).
-template <bool PAR>
+template <bool PAR, class S>
 __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& h, uint64_t start, uint32_t depth,
-                                              Sink& sink)
+                                              S& sink)
 {
     if (h.aux.z & 1u) {
         uint32_t id = h.w.w;
@@ -598,7 +606,8 @@ __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& 
 // Their first 24 bytes from inline_skip came with the extension; the text words are
 // L1 hits next to the window just read.  Pattern bytes are read only past
 // those 24.
-__device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+template <class S>
+__device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h, uint64_t start, S& sink)
 {
     const TrieView& t = a.trie;
     const uint32_t skip = inline_skip(t.filter_k, t.sym_bits);
@@ -637,13 +646,14 @@ __device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h,
 
 // The walking pass (32 warps, 64 registers) keeps the inline check out of
 // line: few of its candidates reach a slot, and inlined it spilled.
-__device__ __noinline__ void emit_inline_call(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+template <class S>
+__device__ __noinline__ void emit_inline_call(const ScanArgs& a, const JumpHit& h, uint64_t start, S& sink)
 {
     emit_inline(a, h, start, sink);
 }
 
-template <bool PAR>
-__device__ __forceinline__ void emit_listed(const ScanArgs& a, const JumpHit& h, uint64_t start, Sink& sink)
+template <bool PAR, class S>
+__device__ __forceinline__ void emit_listed(const ScanArgs& a, const JumpHit& h, uint64_t start, S& sink)
 {
 #ifndef HFB_INLINE_ALL
     if (PAR) {
@@ -654,22 +664,58 @@ __device__ __forceinline__ void emit_listed(const ScanArgs& a, const JumpHit& h,
     emit_inline(a, h, start, sink);
 }
 
-// A start with more records than the registers hold (rare): walk it again and
-// write records kRegRecords.. directly.  Out of line, so each flush carries
-// one copy of the walk.
-template <bool GROUPED, bool IDENT, bool PAR>
-__device__ __noinline__ void rewalk_rest(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
-                                         uint32_t node, uint32_t depth, JumpHit hit, bool at_limit,
+template <bool GROUPED, bool IDENT, int KW, bool PAR, class S>
+__device__ __forceinline__ void run_start(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
+                                          S& sink);
+
+// A start with more records than the registers hold (rare): run it again
+// from its offset and write records kRegRecords.. directly.  Out of line, so
+// each flush carries one copy of the walk, and nothing of the first run
+// (jump slot, node, window) has to stay live for it.
+template <bool GROUPED, bool IDENT, int KW, bool PAR>
+__device__ __noinline__ void rewalk_rest(const ScanArgs& a, const uint16_t* s_sym, uint64_t start,
                                          hepfac_match_t* region, uint64_t at)
 {
-    Sink wr;
-    wr.dst = region;
-    wr.at = at;
-    wr.cap = a.warp_cap;
-    wr.skip = kRegRecords;
-    if (hit.aux.z & kJumpInline) emit_listed<PAR>(a, hit, start, wr);
-    else if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, wr);
-    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, wr, hit.aux.w);
+    WriteSink wr{region, at, a.warp_cap, kRegRecords};
+    run_start<GROUPED, IDENT, KW, PAR>(a, s_sym, start, window_of(raw_window(a, start), start), wr);
+}
+
+// Every record of one start (`win` = text[start, start + 8)): the depth-k
+// jump (byte keys, or packed symbol keys), then the slot's inline list, the
+// depth-limit emit, or a walk from the jump node (from the root without a
+// jump table).
+template <bool GROUPED, bool IDENT, int KW, bool PAR, class S>
+__device__ __forceinline__ void run_start(const ScanArgs& a, const uint16_t* s_sym, uint64_t start, uint64_t win,
+                                          S& sink)
+{
+    uint32_t node = 0, depth = 0;
+    JumpHit hit{};
+    hit.aux.w = kNoId; // no jump: the walk starts at the root with no path id
+    if (KW != 0 && a.trie.jump_bits) {
+        // (grouped records mean sigma > 32: never symbol keys)
+        if (!GROUPED && a.trie.sym_bits && a.packed) {
+            // the key from the packed text (2 loads, not k symbol lookups);
+            // bytes outside the alphabet were packed as symbol 0, so a hit is
+            // checked byte by byte -- by the inline compare itself, or here
+            hit = jump_lookup_key(a.trie, packed_key(a, start), 0u);
+            uint32_t key;
+            if (hit.w.z != kNoId && !(hit.aux.z & kJumpInline) && !symbol_key(a, s_sym, start, key)) hit.w.z = kNoId;
+        } else if (!GROUPED && a.trie.sym_bits) {
+            uint32_t key;
+            if (symbol_key(a, s_sym, start, key)) hit = jump_lookup_key(a.trie, key, 0u);
+            else hit.w.z = kNoId;
+        } else {
+            hit = jump_lookup<KW>(a.trie, win);
+        }
+        node = hit.w.z;
+        depth = a.trie.filter_k;
+    }
+    if (node == kNoId) return;
+    // k == limit: walks end at the jump node; the slot has what they emit
+    const bool at_limit = KW != 0 && a.trie.jump_bits && a.trie.filter_k == a.trie.depth_limit;
+    if (hit.aux.z & kJumpInline) emit_listed<PAR>(a, hit, start, sink);
+    else if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
+    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink, hit.aux.w);
 }
 
 template <bool GROUPED, bool IDENT, int KW, bool PAR>
@@ -716,52 +762,21 @@ struct Walker {
             if (PAR && e < ns) cur = raw_window(a, lo + q[e]);
             Sink sink;
             uint64_t start = 0;
-            uint64_t win = 0;
-            uint32_t node = 0, depth = 0;
-            JumpHit hit{};
-            hit.aux.w = kNoId; // no jump: the walk starts at the root with no path id
-            // k == limit: walks end at the jump node; the slot has what they emit
-            const bool at_limit = KW != 0 && a.trie.jump_bits && a.trie.filter_k == a.trie.depth_limit;
             if (e < ns) {
                 start = lo + q[e];
-                win = window_of(cur, start);
-                if (KW != 0 && a.trie.jump_bits) {
-                    // (grouped records mean sigma > 32: never symbol keys)
-                    if (!GROUPED && a.trie.sym_bits && a.packed) {
-                        // the key from the packed text (2 loads, not k symbol
-                        // lookups); bytes outside the alphabet were packed as
-                        // symbol 0, so a hit is checked byte by byte -- by the
-                        // inline compare itself, or here
-                        hit = jump_lookup_key(a.trie, packed_key(a, start), 0u);
-                        uint32_t key;
-                        if (hit.w.z != kNoId && !(hit.aux.z & kJumpInline) && !symbol_key(a, s_sym, start, key))
-                            hit.w.z = kNoId;
-                    } else if (!GROUPED && a.trie.sym_bits) {
-                        uint32_t key;
-                        if (symbol_key(a, s_sym, start, key)) hit = jump_lookup_key(a.trie, key, 0u);
-                        else hit.w.z = kNoId;
-                    } else {
-                        hit = jump_lookup<KW>(a.trie, win);
-                    }
-                    node = hit.w.z;
-                    depth = a.trie.filter_k;
-                }
-                if (node != kNoId) {
-                    if (hit.aux.z & kJumpInline) emit_listed<PAR>(a, hit, start, sink);
-                    else if (at_limit) emit_at_limit<PAR>(a, hit, start, depth, sink);
-                    else walk<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, sink, hit.aux.w);
-                }
+                run_start<GROUPED, IDENT, KW, PAR>(a, s_sym, start, window_of(cur, start), sink);
             }
             uint32_t tot;
             const uint32_t ex = warp_exclusive(sink.n, lane, tot);
             if (sink.n) {
                 const uint64_t at = cursor + ex;
+                const uint64_t g = a.g0 + start;
                 uint4* dst = reinterpret_cast<uint4*>(region);
-                if (at < a.warp_cap) dst[at] = sink.r0;
-                if (sink.n > 1 && at + 1 < a.warp_cap) dst[at + 1] = sink.r1;
-                if (sink.n > kRegRecords) // rare: re-walk and write the rest directly
-                    rewalk_rest<GROUPED, IDENT, PAR>(a, s_sym, start, win, node, depth, hit, at_limit, region,
-                                                     at + kRegRecords);
+                if (at < a.warp_cap) dst[at] = make_uint4(uint32_t(g), uint32_t(g >> 32), sink.l0, sink.i0);
+                if (sink.n > 1 && at + 1 < a.warp_cap)
+                    dst[at + 1] = make_uint4(uint32_t(g), uint32_t(g >> 32), sink.l1, sink.i1);
+                if (sink.n > kRegRecords) // rare: run the start again and write the rest directly
+                    rewalk_rest<GROUPED, IDENT, KW, PAR>(a, s_sym, start, region, at + kRegRecords);
             }
             cursor += tot;
         }
