@@ -423,10 +423,31 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             prefetch();
 #endif
             if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
-            // final survivors in start order (chunk, lane, position): one warp
-            // scan of the lane's four per-chunk counts packed in 8-bit fields
-            // (exact while every lane has at most 7 survivors in the step)
             const uint32_t n01 = __popc(m01), n23 = __popc(m23);
+            // final survivors in start order (chunk, lane, position).  Common
+            // case (~90% of steps at c3): at most one per lane, placed by one
+            // ballot per chunk.
+            if (!__any_sync(0xFFFFFFFFu, n01 + n23 > 1)) {
+                const uint32_t c0 = __ballot_sync(0xFFFFFFFFu, m01 & 0xFFFFu), c1 = __ballot_sync(0xFFFFFFFFu, m01 >> 16);
+                const uint32_t c2 = __ballot_sync(0xFFFFFFFFu, m23 & 0xFFFFu), c3 = __ballot_sync(0xFFFFFFFFu, m23 >> 16);
+                const uint32_t p1 = __popc(c0), p2 = p1 + __popc(c1), p3 = p2 + __popc(c2);
+                if (m01 | m23) {
+                    const uint32_t j = m01 ? __ffs(m01) - 1 : 32u + __ffs(m23) - 1; // bit in the lane's 64
+                    const uint32_t b = j >> 4;
+                    const uint32_t bal = b == 0 ? c0 : (b == 1 ? c1 : (b == 2 ? c2 : c3));
+                    const uint32_t at = cursor + (b == 0 ? 0u : (b == 1 ? p1 : (b == 2 ? p2 : p3))) + __popc(bal & below);
+                    const uint32_t so = b * kFChunk + 16u * lane + (j & 15u);
+                    if (at < cap) {
+                        region[at] = uint16_t(s * kFStep + so);
+                        keys[at] = staged4(so);
+                    }
+                }
+                cursor += p3 + __popc(c3);
+                continue;
+            }
+            // otherwise one warp scan of the lane's four per-chunk counts
+            // packed in 8-bit fields (exact while every lane has at most 7
+            // survivors in the step)
             const uint32_t cnt = (__popc(m01 & 0xFFFFu)) | ((n01 - __popc(m01 & 0xFFFFu)) << 8) |
                                  (__popc(m23 & 0xFFFFu) << 16) | ((n23 - __popc(m23 & 0xFFFFu)) << 24);
             if (__any_sync(0xFFFFFFFFu, n01 + n23 > 7u)) {
