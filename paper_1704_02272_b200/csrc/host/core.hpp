@@ -8,6 +8,7 @@
 // (csrc/cuda/); nothing here scans text.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <memory>
@@ -15,6 +16,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -34,6 +36,27 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void invalid(const std::string& msg) { fail(HEPFAC_ERR_INVALID_ARG, msg); }
 
 std::string hex_byte(uint8_t b); // "0x4a"-style suffix helper: returns "4a"
+
+// Host compiler threads: HEPFAC_COMPILER_THREADS, else the hardware threads
+// (at most 64).
+unsigned compiler_threads();
+
+// fn(begin, end) over [0, n) in contiguous slices, one per thread; serial
+// below `grain` items.  Results must not depend on the slicing.
+template <typename Fn>
+void parallel_slices(size_t n, size_t grain, Fn&& fn)
+{
+    const unsigned t = unsigned(std::min<size_t>(compiler_threads(), std::max<size_t>(1, n / std::max<size_t>(grain, 1))));
+    if (t <= 1) {
+        fn(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(t);
+    for (unsigned i = 0; i < t; ++i)
+        pool.emplace_back([&, i] { fn(n * i / t, n * (i + 1) / t); });
+    for (auto& th : pool) th.join();
+}
 
 // ---------------------------------------------------------------------------
 // Alphabet: dense byte <-> symbol map (reference alphabet.hpp:13-47).

@@ -17,6 +17,9 @@
 #include "image.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <array>
 #include <cmath>
 #include <cstdlib>
@@ -194,6 +197,15 @@ std::vector<InlineList> inline_lists(const Trie& t, const GpuImage& im, std::vec
 
 GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
 {
+    // HEPFAC_IMAGE_TIMING=1: per-phase wall times on stderr (tuning only)
+    const bool timing = std::getenv("HEPFAC_IMAGE_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](int k) {
+        if (!timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "image phase %d: %.3f s\n", k - 1, std::chrono::duration<double>(now - t_last).count());
+        t_last = now;
+    };
     GpuImage im;
     const uint32_t n = t.node_count;
     if (n >= kMaxGpuNodes) fail(HEPFAC_ERR_NOMEM, "trie too large for the GPU image (>= 2^30 nodes)");
@@ -208,6 +220,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             fail(HEPFAC_ERR_FORMAT, "trie file offset out of range (child run past the node array)");
     }
 
+    phase(0);
     // ---- alphabet --------------------------------------------------------
     im.identity = t.alphabet.is_identity();
     for (unsigned b = 0; b < 256; ++b) {
@@ -216,6 +229,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     }
     im.depth_limit = t.depth_limit.value_or(0);
 
+    phase(1);
     // ---- dictionary + slice-key table -------------------------------------
     const size_t P = t.patterns.size();
     im.pat_off.resize(P);
@@ -258,6 +272,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         im.ht_id[s] = uint32_t(i);
     }
 
+    phase(2);
     // ---- terminal ids: baked in where the node spells exactly one string ----
     std::vector<uint32_t> indeg(n, 0);
     for (uint32_t u = 0; u < n; ++u)
@@ -278,15 +293,20 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     }
     im.term_id.assign(n, kNoId);
-    for (size_t id = 0; id < P; ++id) {
-        uint32_t node = 0;
-        for (unsigned char c : t.patterns[id]) {
-            node = t.transition(node, c);
-            if (node >= n) break;
+    // every pattern's walk, in parallel: a node on a unique path spells one
+    // string, so no two patterns write the same entry
+    parallel_slices(P, 4096, [&](size_t b, size_t e) {
+        for (size_t id = b; id < e; ++id) {
+            uint32_t node = 0;
+            for (unsigned char c : t.patterns[id]) {
+                node = t.transition(node, c);
+                if (node >= n) break;
+            }
+            if (node < n && node != 0 && t.terminal(node) && unique_path[node]) im.term_id[node] = uint32_t(id);
         }
-        if (node < n && node != 0 && t.terminal(node) && unique_path[node]) im.term_id[node] = uint32_t(id);
-    }
+    });
 
+    phase(3);
     // ---- path ids: keyed terminals named by the walk's path ------------------
     // A pattern whose terminal is shared (keyed) is still determined by the
     // deepest path-unique node U on its path when U leads to no other keyed
@@ -301,8 +321,9 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     // the DAG; a cycle disables path ids) equals the number of patterns whose
     // full path ends at a terminal.
     bool dictionary_language = true;
+    std::vector<uint32_t> order; // Kahn (topological) order of the DAG, when it is one
     {
-        std::vector<uint32_t> deg = indeg, order;
+        std::vector<uint32_t> deg = indeg;
         order.reserve(n);
         if (deg[0] != 0) dictionary_language = false;
         else order.push_back(0);
@@ -324,19 +345,24 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 }
             }
         }
-        uint64_t spelled = 0;
-        for (size_t id = 0; id < P && dictionary_language; ++id) {
-            uint32_t node = 0;
-            bool full = true;
-            for (unsigned char c : t.patterns[id]) {
-                node = t.transition(node, c);
-                if (node >= n) {
-                    full = false;
-                    break;
+        std::atomic<uint64_t> spelled{0};
+        if (dictionary_language)
+            parallel_slices(P, 4096, [&](size_t b, size_t e) {
+                uint64_t k = 0;
+                for (size_t id = b; id < e; ++id) {
+                    uint32_t node = 0;
+                    bool full = true;
+                    for (unsigned char c : t.patterns[id]) {
+                        node = t.transition(node, c);
+                        if (node >= n) {
+                            full = false;
+                            break;
+                        }
+                    }
+                    k += (full && node != 0 && t.terminal(node)) ? 1u : 0u;
                 }
-            }
-            spelled += (full && node != 0 && t.terminal(node)) ? 1u : 0u;
-        }
+                spelled += k;
+            });
         dictionary_language = dictionary_language && order.size() == n && terminal_paths == spelled;
     }
     im.dictionary_language = dictionary_language;
@@ -345,25 +371,36 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         for (uint32_t u = 0; u < n; ++u)
             if (unique_path[u]) im.path_id[u] = kNoId;
         std::vector<uint8_t> conflict(n, 0);
-        std::vector<uint32_t> path;
-        for (size_t id = 0; id < P; ++id) {
-            path.assign(1, 0u);
-            for (unsigned char c : t.patterns[id]) {
-                const uint32_t nx = t.transition(path.back(), c);
-                if (nx >= n) break;
-                path.push_back(nx);
+        // each pattern's (U, clean) in parallel, then applied in id order
+        // (the outcome -- one id per U, or a conflict -- is order-independent)
+        std::vector<uint32_t> claim_u(P, kNoId);
+        std::vector<uint8_t> claim_clean(P, 0);
+        parallel_slices(P, 4096, [&](size_t b, size_t e) {
+            std::vector<uint32_t> path;
+            for (size_t id = b; id < e; ++id) {
+                path.assign(1, 0u);
+                for (unsigned char c : t.patterns[id]) {
+                    const uint32_t nx = t.transition(path.back(), c);
+                    if (nx >= n) break;
+                    path.push_back(nx);
+                }
+                const size_t L = path.size() - 1;
+                if (L != t.patterns[id].size()) continue; // truncated away
+                const uint32_t T = path[L];
+                if (!t.terminal(T) || im.term_id[T] != kNoId) continue; // private terminals name themselves
+                size_t u = L;
+                while (u > 0 && !unique_path[path[u]]) --u;
+                if (!unique_path[path[u]]) continue;
+                bool clean = true;
+                for (size_t i = u + 1; i < L; ++i) clean = clean && !t.terminal(path[i]);
+                claim_u[id] = path[u];
+                claim_clean[id] = clean ? 1u : 0u;
             }
-            const size_t L = path.size() - 1;
-            if (L != t.patterns[id].size()) continue; // truncated away
-            const uint32_t T = path[L];
-            if (!t.terminal(T) || im.term_id[T] != kNoId) continue; // private terminals name themselves
-            size_t u = L;
-            while (u > 0 && !unique_path[path[u]]) --u;
-            if (!unique_path[path[u]]) continue;
-            bool clean = true;
-            for (size_t i = u + 1; i < L; ++i) clean = clean && !t.terminal(path[i]);
-            const uint32_t U = path[u];
-            if (!clean || (im.path_id[U] != kNoId && im.path_id[U] != uint32_t(id))) conflict[U] = 1;
+        });
+        for (size_t id = 0; id < P; ++id) {
+            const uint32_t U = claim_u[id];
+            if (U == kNoId) continue;
+            if (!claim_clean[id] || (im.path_id[U] != kNoId && im.path_id[U] != uint32_t(id))) conflict[U] = 1;
             else im.path_id[U] = uint32_t(id);
         }
         for (uint32_t u = 0; u < n; ++u)
@@ -372,6 +409,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     // the path id a walk carries after entering node v from a parent carrying `pend`
     auto pend_at = [&](uint32_t v, uint32_t pend) { return im.path_id[v] != kKeep ? im.path_id[v] : pend; };
 
+    phase(4);
     // ---- buckets: CSR, each sorted by (length, id) -----------------------
     im.bucket_of.assign(n, kNoId);
     for (const auto& [node, ids] : t.buckets) {
@@ -393,6 +431,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     if (im.bk_span.empty()) im.bk_span.assign(2, 0);
     if (im.bk_entry.empty()) im.bk_entry.assign(4, 0);
 
+    phase(5);
     // ---- node records ------------------------------------------------------
     const uint32_t sigma = t.alphabet.size();
     im.groups = sigma <= 32 ? 0 : (sigma + 63) / 64;
@@ -401,28 +440,33 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     };
     if (im.groups == 0) {
         im.nodes.resize(size_t(n) * 2);
-        for (uint32_t u = 0; u < n; ++u) {
-            im.nodes[2 * size_t(u)] = t.cell(u)[0];
-            im.nodes[2 * size_t(u) + 1] = (kids[u] ? t.offset(u) : 0u) | flags(u);
-        }
+        parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+            for (size_t u = b; u < e; ++u) {
+                im.nodes[2 * u] = t.cell(uint32_t(u))[0];
+                im.nodes[2 * u + 1] = (kids[u] ? t.offset(uint32_t(u)) : 0u) | flags(uint32_t(u));
+            }
+        });
     } else {
         im.nodes.resize(size_t(n) * im.groups * 4);
-        for (uint32_t u = 0; u < n; ++u) {
-            const uint32_t* c = t.cell(u);
-            uint32_t base = kids[u] ? t.offset(u) : 0u;
-            for (uint32_t g = 0; g < im.groups; ++g) {
-                const uint32_t w0 = 2 * g < t.words ? c[2 * g] : 0u;
-                const uint32_t w1 = 2 * g + 1 < t.words ? c[2 * g + 1] : 0u;
-                uint32_t* r = &im.nodes[(size_t(u) * im.groups + g) * 4];
-                r[0] = w0;
-                r[1] = w1;
-                r[2] = (base & kBaseMask) | flags(u);
-                r[3] = im.term_id[u];
-                base += uint32_t(__builtin_popcount(w0) + __builtin_popcount(w1));
+        parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+            for (size_t u = b; u < e; ++u) {
+                const uint32_t* c = t.cell(uint32_t(u));
+                uint32_t base = kids[u] ? t.offset(uint32_t(u)) : 0u;
+                for (uint32_t g = 0; g < im.groups; ++g) {
+                    const uint32_t w0 = 2 * g < t.words ? c[2 * g] : 0u;
+                    const uint32_t w1 = 2 * g + 1 < t.words ? c[2 * g + 1] : 0u;
+                    uint32_t* r = &im.nodes[(u * im.groups + g) * 4];
+                    r[0] = w0;
+                    r[1] = w1;
+                    r[2] = (base & kBaseMask) | flags(uint32_t(u));
+                    r[3] = im.term_id[u];
+                    base += uint32_t(__builtin_popcount(w0) + __builtin_popcount(w1));
+                }
             }
-        }
+        });
     }
 
+    phase(6);
     // ---- report depths: min_emit (BFS) -------------------------------------
     {
         std::vector<uint32_t> depth(n, UINT32_MAX), q{0};
@@ -443,12 +487,24 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         if (im.depth_limit && !t.buckets.empty()) im.min_emit = std::min(im.min_emit, im.depth_limit);
     }
 
+    phase(7);
     // ---- reach: longest root path (cyclic => unbounded), plus buckets ------
     if (im.depth_limit) {
         uint64_t r = im.depth_limit;
         for (const auto& [node, ids] : t.buckets)
             for (uint32_t id : ids) r = std::max<uint64_t>(r, im.pat_len[id]);
         im.reach = r;
+    } else if (order.size() == n) {
+        // acyclic (Kahn order covers every node): longest path in reverse
+        // topological order
+        std::vector<uint64_t> longest(n, 0);
+        for (size_t h = n; h-- > 0;) {
+            const uint32_t u = order[h];
+            uint64_t best = 0;
+            for (uint32_t k = 0; k < kids[u]; ++k) best = std::max(best, 1 + longest[t.offset(u) + k]);
+            longest[u] = best;
+        }
+        im.reach = longest[0];
     } else {
         // iterative DFS post-order over the reachable graph
         std::vector<uint64_t> longest(n, 0);
@@ -476,6 +532,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         im.reach = cyclic ? UINT64_MAX : longest[0];
     }
 
+    phase(8);
     // ---- start filter --------------------------------------------------------
     if (im.min_emit != UINT32_MAX) {
         const uint32_t k = std::min(im.min_emit, kMaxFilterKey);
@@ -663,6 +720,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     }
 
+    phase(9);
     // ---- symbol-key mode (small alphabets) -----------------------------------
     // Byte keys carry log2(sigma) bits per byte: 8 bytes of DNA are 16 bits, of
     // a binary alphabet 8.  When the shortest report depth allows more than 8
@@ -749,6 +807,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             }
         }
     }
+    phase(10);
     // ---- direct-index form (filter mode 5, layout.hpp) -------------------------
     // Alphabets of at most 4 symbols whose every pattern has 8..32 symbols
     // (c2: DNA, 10k patterns of 8-32): the byte-key path filters on 8-byte
@@ -824,6 +883,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     }
 
+    phase(11);
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
     if (im.jump.empty()) im.jump.assign(kJumpWords, 0u), im.jump_ext.clear();

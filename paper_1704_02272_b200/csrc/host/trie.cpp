@@ -24,9 +24,6 @@
 
 namespace hfb {
 
-namespace {
-
-// Host compiler threads: HEPFAC_COMPILER_THREADS, else the hardware threads.
 unsigned compiler_threads()
 {
     if (const char* s = std::getenv("HEPFAC_COMPILER_THREADS")) {
@@ -36,22 +33,7 @@ unsigned compiler_threads()
     return std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
 }
 
-// fn(begin, end) over [0, n) in contiguous slices, one per thread; serial
-// below `grain` items.  Results must not depend on the slicing.
-template <typename Fn>
-void parallel_slices(size_t n, size_t grain, Fn&& fn)
-{
-    const unsigned t = unsigned(std::min<size_t>(compiler_threads(), std::max<size_t>(1, n / std::max<size_t>(grain, 1))));
-    if (t <= 1) {
-        fn(size_t(0), n);
-        return;
-    }
-    std::vector<std::thread> pool;
-    pool.reserve(t);
-    for (unsigned i = 0; i < t; ++i)
-        pool.emplace_back([&, i] { fn(n * i / t, n * (i + 1) / t); });
-    for (auto& th : pool) th.join();
-}
+namespace {
 
 // Stable order of `v` under `less`, sorted in parallel slices and merged
 // pairwise (the result equals std::stable_sort's).

@@ -287,3 +287,23 @@ def test_error_statuses_equal_reference(lib, ref):
             assert out[0][0] != "ok"
             continue
         assert out[0] == out[1], (i, out)
+
+
+def test_million_pattern_compile_time(lib):
+    # the host trie compiler for config 5's largest set
+    # (1M byte patterns, len 4-32): build, stage-2 compression and the GPU
+    # image (its reach, through hepfac_b200_halo, which needs no device).
+    # The reference takes ~10 s to build and ~33 s to compress (SURVEY 8(a)
+    # rows a3, a5); here each step runs on all host threads.
+    import time
+    w = workloads.config("c5", count=1_000_000)
+    a = lib.alphabet(256)
+    t0 = time.perf_counter()
+    t = lib.build_trie(lib.patterns(w.patterns, a))
+    t1 = time.perf_counter()
+    s2, st = t.compress(2)
+    t2 = time.perf_counter()
+    halo = lib.halo(s2)
+    t3 = time.perf_counter()
+    assert st.nodes_before == 16041198 and s2.node_count() == 13192775 and halo == 31
+    assert t3 - t0 < 90, (t1 - t0, t2 - t1, t3 - t2)
