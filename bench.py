@@ -430,7 +430,7 @@ def main():
     dominant_s = first_s + second_s if direct else first_s
     achieved = alg_bytes / dominant_s / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config, owned),
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(w.name, owned),
                 "peak_source": peak_src,
                 "kernel": ("pfac_pack_dna_kernel + pfac_dna_kernel (the whole step)" if direct else
                            {2: "pfac_pair_filter_kernel (filter pass)",
