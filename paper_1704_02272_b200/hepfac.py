@@ -204,8 +204,9 @@ class Library:
         self.is_b200 = hasattr(self.dll, "hepfac_b200_device_count")
         if self.is_b200:
             for name, res, args in _B200_PROTOTYPES:
-                fn = getattr(self.dll, name)
-                fn.restype, fn.argtypes = res, args
+                fn = getattr(self.dll, name, None)  # (an older build may lack a later addition)
+                if fn is not None:
+                    fn.restype, fn.argtypes = res, args
 
     # -- plumbing ---------------------------------------------------------
     def check(self, status: int):
