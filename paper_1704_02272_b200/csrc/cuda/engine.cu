@@ -553,7 +553,7 @@ struct Workspace {
     // streamed hepfac_scan: D2H of each chunk's records on their own stream,
     // a pinned staging ring for pageable callers, per-chunk count mirrors
     cudaStream_t d2h = nullptr;
-    static constexpr int kStages = 3;
+    static constexpr int kStages = 4;
     uint8_t* h_stage[kStages] = {};
     size_t h_stage_cap = 0;
     cudaEvent_t stage_done[kStages] = {};
@@ -1062,7 +1062,7 @@ private:
 
 void par_memcpy(void* dst, const void* src, size_t n)
 {
-    const size_t kSlice = size_t(4) << 20;
+    const size_t kSlice = size_t(256) << 10; // per helper thread at least
     const unsigned T = unsigned(std::min<size_t>(copy_threads(), std::max<size_t>(1, n / kSlice)));
     if (T <= 1) {
         std::memcpy(dst, src, n);
@@ -1075,6 +1075,23 @@ void par_memcpy(void* dst, const void* src, size_t n)
         const size_t lo = (n * i / T) & ~size_t(4095), hi = i + 1 == T ? n : (n * (i + 1) / T) & ~size_t(4095);
         std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo, hi - lo);
     });
+}
+
+// Staging piece for pageable text: a text's eighth, between 2 and 16 MiB
+// (HEPFAC_STAGE_MIB overrides).  Measured on the B200 host (16 threads, 60 MB
+// L3; c3 4 GiB / c2 1 GiB / c1 16 MiB, Gbps through hepfac_scan): 2 MiB
+// 211 / 210 / 178, 4 MiB 354 / 331 / 77, 8 MiB 414 / 368 / 66, 16 MiB 424 /
+// 387 / 61, 64 MiB 374 / 303 / 59 -- against 434 / 431 / 323 from pinned
+// text.  Small pieces pay the copy threads' wake-up per piece; whole chunks
+// leave the copy and the DMA of a chunk unoverlapped.
+uint64_t stage_piece_bytes(uint64_t text_bytes)
+{
+    if (const char* s = std::getenv("HEPFAC_STAGE_MIB")) {
+        const long v = std::strtol(s, nullptr, 10);
+        if (v >= 1 && v <= 1024) return uint64_t(v) << 20;
+    }
+    const uint64_t eighth = ((text_bytes + 7) / 8 + 0xFFFFF) & ~uint64_t(0xFFFFF);
+    return std::clamp<uint64_t>(eighth, uint64_t(2) << 20, uint64_t(16) << 20);
 }
 
 // Pageable (not page-locked, not device) memory goes through the staging
@@ -1094,23 +1111,22 @@ bool is_pageable(const void* p)
 // slots while the previous chunk's launch runs on the compute stream; each
 // launch places its records right after the previous chunk's (device-side
 // running base), so the output is ordered without host syncs between chunks.
-// Pageable text is first copied (several host threads) into a ring of
-// kStages pinned buffers, so the DMA runs at pinned speed and the host copy
-// of chunk c+1 overlaps the DMA of chunk c.  With a `sink`, chunk c's records
+// Pageable text is copied (several host threads) piece by piece into a ring
+// of kStages small pinned buffers, each piece's DMA queued as soon as it is
+// copied, so the host copy of piece p+1 overlaps the DMA of piece p.  With a
+// `sink`, chunk c's records
 // go D2H (own stream) into the sink as soon as its kernel has finished,
 // overlapping chunks c+1...; without one they stay in ws.d_out.
 uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, uint64_t avail, uint64_t owned,
                      uint64_t g0, uint64_t halo, MatchList* sink, ScanStats& st)
 {
     const bool stage = is_pageable(text);
-    // Staged (pageable) text: at least ~8 chunks of >= 4 MiB, so the host
-    // copy of chunk c+1 overlaps the DMA of chunk c even for small texts.
-    uint64_t C = stream_chunk_bytes();
-    if (stage) C = std::min(C, std::max<uint64_t>(uint64_t(4) << 20, ((owned + 7) / 8 + 0xFFFFF) & ~uint64_t(0xFFFFF)));
+    const uint64_t C = stream_chunk_bytes();
     const uint64_t n = (owned + C - 1) / C;
     const uint64_t slot_bytes = std::min(avail, C + halo);
+    const uint64_t piece = stage_piece_bytes(avail);
     ws.ensure_slots(slot_bytes);
-    if (stage) ws.ensure_staging(slot_bytes);
+    if (stage) ws.ensure_staging(piece);
     ws.regrow(ws.d_bases, ws.bases_cap, n + 1);
     ws.ensure_host_bases(n + 1);
     if (ws.out_cap < initial_records(owned)) ws.ensure_out(initial_records(owned));
@@ -1123,6 +1139,7 @@ uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, u
         CK(cudaEventRecord(ws.ev[0], ws.stream));
         CK(cudaStreamWaitEvent(ws.copy, ws.ev[0], 0));
         bool overflow = false;
+        uint64_t pieces = 0; // staged pieces queued so far (ring position)
         // chunk k's base and overflow words are on the host once cnt_done fires
         auto drain = [&](uint64_t k) {
             const int slot = int(k & 1);
@@ -1149,16 +1166,21 @@ uint64_t stream_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* text, u
             const int slot = int(c & 1);
             const uint64_t lo = c * C, own = std::min(C, owned - lo), bytes = std::min(avail - lo, own + halo);
             const uint8_t* src = text + lo;
-            if (stage) {
-                const int r = int(c % Workspace::kStages);
-                if (c >= uint64_t(Workspace::kStages)) CK(cudaEventSynchronize(ws.stage_done[r]));
-                par_memcpy(ws.h_stage[r], src, size_t(bytes));
-                src = ws.h_stage[r];
-            }
             if (c >= 2) CK(cudaStreamWaitEvent(ws.copy, ws.kern_done[slot], 0));
-            CK(cudaMemcpyAsync(ws.d_slot[slot], src, size_t(bytes), cudaMemcpyDefault, ws.copy));
+            if (stage) {
+                for (uint64_t off = 0; off < bytes; off += piece, ++pieces) {
+                    const uint64_t len = std::min(piece, bytes - off);
+                    const int r = int(pieces % Workspace::kStages);
+                    if (pieces >= uint64_t(Workspace::kStages)) CK(cudaEventSynchronize(ws.stage_done[r]));
+                    par_memcpy(ws.h_stage[r], src + off, size_t(len));
+                    CK(cudaMemcpyAsync(ws.d_slot[slot] + off, ws.h_stage[r], size_t(len), cudaMemcpyHostToDevice,
+                                       ws.copy));
+                    CK(cudaEventRecord(ws.stage_done[r], ws.copy));
+                }
+            } else {
+                CK(cudaMemcpyAsync(ws.d_slot[slot], src, size_t(bytes), cudaMemcpyDefault, ws.copy));
+            }
             CK(cudaEventRecord(ws.h2d_done[slot], ws.copy));
-            if (stage) CK(cudaEventRecord(ws.stage_done[c % Workspace::kStages], ws.copy));
             CK(cudaStreamWaitEvent(ws.stream, ws.h2d_done[slot], 0));
             if (c == 0) CK(cudaEventRecord(ws.ev[1], ws.stream));
             st.kernel_launches +=

@@ -313,9 +313,12 @@ def test_streamed_scan_equals_resident(gpu, monkeypatch, sigma, stages, depth, t
     assert same(got, want)
     monkeypatch.setenv("HEPFAC_CHUNK_MIB", "64")
     assert same(gpu.scan(t, tx), want)
-    # pageable text is staged in >= 4 MiB chunks (at least ~8 per text)
+    # one 64 MiB chunk; the pageable text is staged through the pinned ring
+    # in pieces (2 MiB here, and HEPFAC_STAGE_MIB=1: six pieces)
     st = gpu.last_scan_stats()
-    assert st["staged"] and st["chunks"] == -(-tx.size // (4 << 20))
+    assert st["staged"] and st["chunks"] == 1
+    monkeypatch.setenv("HEPFAC_STAGE_MIB", "1")
+    assert same(gpu.scan(t, tx), want)
 
 
 @pytest.mark.parametrize("stages,depth", [(1, 4), (2, None)])
