@@ -75,20 +75,31 @@ int pick_device()
 }
 
 // Dynamic shared memory is a per-kernel-function attribute, and every trie
-// with the same kernel choice shares one instantiation, so a per-trie size
-// would let a small trie lower the cap below what a bigger trie's launch
-// needs.  The cap is set once to the device's opt-in maximum instead (the
-// value is the same for every caller, so concurrent setters cannot race it
-// down); each launch still passes its own trie's size.
+// with the same kernel choice shares one instantiation: a cap set per trie
+// at image time let a small trie lower it below a bigger trie's need (ADVICE
+// r1).  Every launch sets the cap to its own trie's size, under one lock
+// held across the set and the launch, so concurrent callers with different
+// tries cannot lower it between another caller's set and launch, and each
+// kernel runs with exactly the shared memory its trie asks for.
+std::mutex g_smem_mu;
+
+struct SmemLaunch {
+    std::lock_guard<std::mutex> lk{g_smem_mu};
+    template <typename F>
+    SmemLaunch(F* fn, size_t bytes)
+    {
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(bytes)));
+    }
+};
+
 template <typename F>
-void allow_max_smem(F* fn, int device)
+int occupancy(F* fn, int threads, size_t smem)
 {
-    int optin = 0;
-    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    cudaFuncAttributes fa{};
-    CK(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)));
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            optin - int(fa.sharedSizeBytes)));
+    SmemLaunch cap(fn, smem);
+    int n = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    return n;
 }
 
 template <typename T>
@@ -439,17 +450,13 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
         d->dna_warps = wide ? 32u : 16u;
         d->dna_kernel = wide ? gpu::pfac_dna_kernel<32> : gpu::pfac_dna_kernel<16>;
         d->dna_smem = gpu::dna_smem_bytes(im.dna_keys, im.dna_pats, d->dna_warps);
-        allow_max_smem(d->dna_kernel, device);
-        int bps = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, d->dna_kernel, int(d->dna_warps * 32), d->dna_smem));
-        d->dna = bps >= 1;
+        d->dna = occupancy(d->dna_kernel, int(d->dna_warps * 32), d->dna_smem) >= 1;
     }
 
     // one-pass (fused) kernel: always available
     d->kernel = select_kernel(d->grouped, d->identity, d->kw, im.filter_mode == 2);
     d->smem = size_t(v.filter_words) * 4 + gpu::smem_fixed_bytes(false);
-    allow_max_smem(d->kernel, device);
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->blocks_per_sm, d->kernel, int(d->warps * 32), d->smem));
+    d->blocks_per_sm = occupancy(d->kernel, int(d->warps * 32), d->smem);
     d->blocks_per_sm = std::max(1, d->blocks_per_sm);
     // two-pass pipeline (always for symbol keys: the one-pass kernel reads byte keys)
     d->sym_bits = im.sym_bits;
@@ -472,9 +479,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
-        allow_max_smem(d->walk_kernel, device);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->walk_blocks_per_sm, d->walk_kernel,
-                                                         int(gpu::kCWarps * 32), d->walk_smem));
+        d->walk_blocks_per_sm = occupancy(d->walk_kernel, int(gpu::kCWarps * 32), d->walk_smem);
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         if (im.filter_mode == 4) // the whole shared-memory level, nothing else
             d->filter_smem = size_t(v.filter_l1_words) * 4;
@@ -483,9 +488,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
                              (im.filter_mode == 3 ? 0
                                                   : (pair_queue_form() ? gpu::filter_smem_fixed_bytes()
                                                                        : gpu::filter2_smem_fixed_bytes()));
-        allow_max_smem(d->filter_fn, device);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d->filter_blocks_per_sm, d->filter_fn, gpu::kFThreads,
-                                                         d->filter_smem));
+        d->filter_blocks_per_sm = occupancy(d->filter_fn, int(gpu::kFThreads), d->filter_smem);
         if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
     }
     CK(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -869,8 +872,11 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
             f.packed = ws.d_packed;
             a.packed = ws.d_packed;
         }
-        dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
-        CK(cudaGetLastError());
+        {
+            SmemLaunch cap(dt.filter_fn, dt.filter_smem);
+            dt.filter_fn<<<unsigned(fgrid), gpu::kFThreads, dt.filter_smem, ws.stream>>>(f);
+            CK(cudaGetLastError());
+        }
         if (between) CK(cudaEventRecord(between, ws.stream));
         // the single + L2 filter pass already tested the L2 bitmap
         if (dt.filter_mode == 4) a.trie.filter2_bits = 0;
@@ -903,6 +909,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         a.packed = ws.d_packed;
         a.valid = ws.d_packed + 2 * vw;
         void* dparams[] = {&a};
+        SmemLaunch cap(dt.dna_kernel, dt.dna_smem);
         const cudaError_t de = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dt.dna_kernel),
                                                            dim3(unsigned(l.grid)), dim3(dt.dna_warps * 32), dparams,
                                                            dt.dna_smem, ws.stream);
@@ -913,6 +920,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         return 2;
     }
     void* params[] = {&a};
+    SmemLaunch cap(two ? dt.walk_kernel : dt.kernel, two ? dt.walk_smem : dt.smem);
     const cudaError_t e = cudaLaunchCooperativeKernel(
         reinterpret_cast<const void*>(two ? dt.walk_kernel : dt.kernel), dim3(unsigned(l.grid)),
         dim3((two ? gpu::kCWarps : dt.warps) * 32), params, two ? dt.walk_smem : dt.smem, ws.stream);
