@@ -433,6 +433,7 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(w.name, owned),
                 "peak_source": peak_src,
                 "kernel": ("pfac_pack_dna_kernel + pfac_dna_kernel (the whole step)" if direct else
+                           "pfac_l2_filter_kernel (filter pass)" if info["filter_mode"] == 4 and pipeline else
                            {2: "pfac_pair_filter_kernel (filter pass)",
                             3: "pfac_pack_symbols_kernel + pfac_symbol_filter_kernel (filter pass)"}
                            .get(kernels_per_scan, "pfac_scan_kernel (fused)")),

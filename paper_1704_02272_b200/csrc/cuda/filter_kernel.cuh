@@ -601,8 +601,10 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __gr
                 const uint32_t key = f_key<KW>(w, j, mhi);
                 const uint32_t word = s_tab[__umulhi(key * kFilterMul, words)]; // filter_l1_word
                 const bool hit = ((valid >> j) & 1u) && int32_t(word << (key & 31u)) < 0;
-                const uint32_t s2 = filter2_hash(key) >> sh2;
-                w2[j] = hit ? probe_l2(l2 + (s2 >> 5)) >> (s2 & 31u) : 0u;
+                const uint32_t h2 = filter2_hash(key), s2 = h2 >> sh2;
+                // both of the key's bits in its L2 word (image.cpp, mode 4)
+                w2[j] = hit ? probe_l2(l2 + (s2 >> 5)) : 0u;
+                w2[j] = (w2[j] >> (s2 & 31u)) & (w2[j] >> (h2 & 31u));
             }
 #pragma unroll
             for (int j = 0; j < 16; ++j) m |= (w2[j] & 1u) << j;
