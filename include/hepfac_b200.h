@@ -99,6 +99,7 @@ typedef struct hepfac_b200_layout_info {
     uint32_t filter_mode;     /* 0 none, 1 single probe per start, 2 pair probes (one per two starts),
                                  3 packed-symbol keys, 4 single probe + L2-resident bitmap (two-pass) */
     uint32_t filter_pass_ppm; /* estimated random starts per million that reach the walk queue */
+    uint32_t filter2_bits;    /* log2 bits of the L2-resident filter level; 0 = none */
 } hepfac_b200_layout_info_t;
 
 hepfac_status_t hepfac_b200_layout_info(const hepfac_trie_t* trie, hepfac_b200_layout_info_t* out);

@@ -475,7 +475,9 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
             if (im.filter_mode == 4)
                 d->filter_fn = d->kw == 3 ? gpu::pfac_l2_filter_kernel<3> : gpu::pfac_l2_filter_kernel<2>;
             else
-                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_queue_kernel : gpu::pfac_pair_filter_kernel;
+                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_queue_kernel
+                                                 : (v.filter2_bits ? gpu::pfac_pair_filter_kernel<true>
+                                                                   : gpu::pfac_pair_filter_kernel<false>);
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
@@ -861,7 +863,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         f.cand_need = ws.d_small + 5;
         f.filter_k = dt.view.filter_k;
         f.table2 = dt.view.filter2;
-        f.table2_bits = dt.view.filter2_bits;
+        f.table2_bits = dt.view.filter2_bits; // 0 when the image has no L2 level
         if (dt.sym_bits) {
             const uint64_t per = 32 / dt.sym_bits, words = (n_avail + per - 1) / per;
             ws.regrow(ws.d_packed, ws.packed_cap, words + 4);
@@ -878,8 +880,9 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
             CK(cudaGetLastError());
         }
         if (between) CK(cudaEventRecord(between, ws.stream));
-        // the single + L2 filter pass already tested the L2 bitmap
-        if (dt.filter_mode == 4) a.trie.filter2_bits = 0;
+        // the filter pass already tested the L2 bitmap (single + L2; and the
+        // pair filter pass, which tests both bits of its survivors)
+        if (dt.filter_mode == 4 || (dt.filter_mode == 2 && !pair_queue_form())) a.trie.filter2_bits = 0;
         a.cand = ws.d_cand;
         a.cand_key = ws.d_cand_key;
         a.cand_cap = ws.cand_cap;
@@ -1426,6 +1429,7 @@ LayoutInfo layout_info(const Trie& t)
     li.keyed_terminals = d->keyed_terminals;
     li.filter_mode = d->dna ? 5u : (d->kw == 0 ? 0u : (d->filter_mode == 5 ? 1u : d->filter_mode));
     li.filter_pass_ppm = uint32_t(std::min(1.0, d->filter_pass) * 1e6);
+    li.filter2_bits = d->view.filter2_bits;
     return li;
 }
 

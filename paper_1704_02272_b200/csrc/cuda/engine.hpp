@@ -76,7 +76,7 @@ struct LayoutInfo {
     uint32_t node_count, groups, record_bytes, filter_k, filter_bits, min_emit, smem_bytes,
         blocks_per_sm, sm_count, identity;
     uint64_t filter_paths, reach, device_bytes, private_terminals, keyed_terminals;
-    uint32_t filter_mode, filter_pass_ppm;
+    uint32_t filter_mode, filter_pass_ppm, filter2_bits;
 };
 LayoutInfo layout_info(const Trie& t);
 

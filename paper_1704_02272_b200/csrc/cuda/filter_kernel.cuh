@@ -276,6 +276,9 @@ __device__ __forceinline__ uint32_t f_pair_probe(const uint32_t* __restrict__ ta
     return tab[(mid * kPairMul) >> shift];
 }
 
+// L2: the image has an L2-resident third level (dense pair survivors); a
+// separate instantiation keeps the common case's code unchanged.
+template <bool L2>
 __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __grid_constant__ FilterArgs a)
 {
     extern __shared__ __align__(128) uint8_t fsmem[];
@@ -343,15 +346,21 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
 #if defined(HFB_LATE_PREFETCH) && !HFB_LATE_PREFETCH
             prefetch();
 #endif
-            // the word after the step (lane 0 of the next step's first chunk)
-            uint32_t tail = 0;
-            if (lane == 31 && sbase + kFStep < avail16)
-                tail = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
+            // the 4 bytes after the step (8 with the third level: its keys
+            // reach 8 bytes past a start)
+            uint2 tail = make_uint2(0u, 0u);
+            if (lane == 31 && sbase + kFStep < avail16) {
+                if (L2) tail = __ldg(reinterpret_cast<const uint2*>(a.text + sbase + kFStep));
+                else tail.x = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
+            }
             __syncwarp(); // the previous step's staged bytes are no longer read
 #pragma unroll
             for (uint32_t b = 0; b < kFChunks; ++b)
                 *reinterpret_cast<uint4*>(stage + b * kFChunk + 16u * lane) = cur[b];
-            if (lane == 31) *reinterpret_cast<uint32_t*>(stage + kFStep) = tail;
+            if (lane == 31) {
+                if (L2) *reinterpret_cast<uint2*>(stage + kFStep) = tail;
+                else *reinterpret_cast<uint32_t*>(stage + kFStep) = tail.x;
+            }
             __syncwarp();
 
             const bool full = (s + 1) * kFStep <= rem; // warp-uniform: every start of the step may report
@@ -418,6 +427,42 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                 }
                 m01 &= ~fail01;
                 m23 &= ~fail23;
+            }
+            // third level (dictionaries whose pair survivors are dense, e.g. c5
+            // 100k: 3.6% of starts): both bits of the start's k-byte key in the
+            // L2-resident bitmap (image.cpp), four survivors' loads in flight
+            // per round, before the survivors are written out.  Conservative:
+            // it only removes starts no dictionary path begins with.
+            if (L2 && __any_sync(0xFFFFFFFFu, m01 | m23)) {
+                const uint32_t sh2 = 32u - a.table2_bits, base = 16u * lane;
+                const uint32_t k = a.filter_k;
+                const uint32_t mhi = k >= 8 ? 0xFFFFFFFFu : (k > 4 ? ((1u << (8 * (k - 4))) - 1u) : 0u);
+                uint64_t left = (uint64_t(m23) << 32) | m01, fail = 0;
+                while (__any_sync(0xFFFFFFFFu, left != 0)) {
+                    uint32_t w2[4], h2[4], jj[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        w2[r] = 0xFFFFFFFFu, h2[r] = 0u, jj[r] = 64u;
+                        if (left) {
+                            uint32_t j;
+                            asm("bfind.u64 %0, %1;" : "=r"(j) : "l"(left));
+                            left ^= 1ull << j;
+                            const uint32_t so = base + (j & 15u) + (j >> 4) * kFChunk;
+                            uint32_t key = staged4(so);
+                            if (mhi) key += (staged4(so + 4) & mhi) * 0x85EBCA77u; // filter_fold
+                            const uint32_t h = filter2_hash(key);
+                            h2[r] = ((h >> sh2) & 31u) | ((h & 31u) << 8);
+                            w2[r] = __ldg(a.table2 + ((h >> sh2) >> 5));
+                            jj[r] = j;
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (jj[r] < 64u && !((w2[r] >> (h2[r] & 31u)) & (w2[r] >> (h2[r] >> 8)) & 1u))
+                            fail |= 1ull << jj[r];
+                }
+                m01 &= ~uint32_t(fail);
+                m23 &= ~uint32_t(fail >> 32);
             }
 #if !defined(HFB_LATE_PREFETCH) || HFB_LATE_PREFETCH
             prefetch();

@@ -682,6 +682,10 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 for (uint64_t g : grams) {
                     const uint32_t s2 = filter2_slot(filter_fold(g), bits2);
                     im.filter2[s2 >> 5] |= 1u << (s2 & 31);
+                    // pair tries: a second bit in the same word (the hash's low
+                    // bits) for the filter pass's two-bit test; single-bit
+                    // probes of the same table stay conservative
+                    if (im.filter_mode == 2) im.filter2[s2 >> 5] |= 1u << (filter2_hash(filter_fold(g)) & 31u);
                 }
             }
             // Saturated first level (dictionaries of ~10^6 k-grams: 2^20 bits

@@ -91,7 +91,7 @@ class _LayoutInfo(C.Structure):
                                           "min_emit", "smem_bytes", "blocks_per_sm", "sm_count", "identity")] + \
                [(n, C.c_uint64) for n in ("filter_paths", "reach", "device_bytes", "private_terminals",
                                           "keyed_terminals")] + \
-               [(n, C.c_uint32) for n in ("filter_mode", "filter_pass_ppm")]
+               [(n, C.c_uint32) for n in ("filter_mode", "filter_pass_ppm", "filter2_bits")]
 
 
 _P = C.c_void_p

@@ -32,7 +32,7 @@ prof() { # name, kernel regex, launches to capture, mangled kernel name for the 
         > $out/ncu_${name}_lines.txt 2>&1
     rm -f /tmp/ncu_$name.ncu-rep
 }
-prof c3_filter pfac_pair_filter_kernel 1 _ZN3hfb3gpu23pfac_pair_filter_kernelENS0_10FilterArgsE --bytes-per-gpu $G
+prof c3_filter pfac_pair_filter_kernel 1 _ZN3hfb3gpu23pfac_pair_filter_kernelILb0EEEvNS0_10FilterArgsE --bytes-per-gpu $G
 prof c3_walk 'pfac_scan_kernel' 1 _ZN3hfb3gpu16pfac_scan_kernelILb1ELb1ELi3ELb0ELb1EEEvNS0_8ScanArgsE --bytes-per-gpu $G
 prof c2_dna 'pfac_dna_kernel' 1 _ZN3hfb3gpu15pfac_dna_kernelILj32EEEvNS0_8ScanArgsE --config c2 --bytes-per-gpu $G
 prof c2_pack 'pfac_pack_dna' 1 _ZN3hfb3gpu20pfac_pack_dna_kernelILb1EEEvPKhmPKtjPjS6_m --config c2 --bytes-per-gpu $G

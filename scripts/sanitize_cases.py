@@ -71,6 +71,8 @@ CASES = {
                                   env={"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_QUEUE": "1"}),
     "two_pass_inlane": lambda: run("two_pass_inlane", 256, 300, 4, 20, 1 << 20,
                                    env={"HEPFAC_PIPELINE_MIN_MIB": "0"}),
+    "two_pass_pair_l2": lambda: run("two_pass_pair_l2", 256, 30000, 4, 24, 1 << 16,
+                                    env={"HEPFAC_PIPELINE_MIN_MIB": "0"}),
     "two_pass_l2": lambda: run("two_pass_l2", 256, 300, 4, 20, 1 << 20, env={"HEPFAC_PIPELINE_MIN_MIB": "0",
                                                                             "HEPFAC_FILTER_MODE": "l2"}),
     "symbol": lambda: run("symbol", 4, 200, 12, 24, 1 << 20, stages=2),

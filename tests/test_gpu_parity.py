@@ -345,6 +345,29 @@ def test_pair_pipeline_all_starts_pass(gpu, monkeypatch, stages, depth, mode, co
     assert same(got, oracle.naive_find_all(tx, pats))
 
 
+@pytest.mark.parametrize("count,lo", [(30000, 4), (60000, 5)])
+def test_pair_filter_with_l2_level(gpu, ref, monkeypatch, count, lo):
+    # Pair tries whose pair survivors are dense (c5 100k: 3.6% of starts)
+    # get an L2-resident third level that the filter pass tests on its
+    # survivors (two bits per key); k = 4 and k = 5 (8-byte key reads from
+    # the staged step).  The walking pass then skips its own L2 probe.
+    monkeypatch.setenv("HEPFAC_PIPELINE_MIN_MIB", "0")
+    rng = np.random.default_rng(count + lo)
+    a, syms = alphabet_bytes(gpu, 256)
+    pats = pattern_set(rng, syms, count, lo, 24)
+    tx = text(rng, syms, (1 << 21) + 77)
+    for i in range(0, tx.size - 40, 977):
+        plant(tx, pats[i % len(pats)], i)
+    # (the naive oracle is O(text x patterns): the compiled reference instead)
+    want = ref.scan(ref.build_trie(ref.patterns(pats, ref.alphabet(256))), tx, workers=os.cpu_count())
+    assert want.size > 2000
+    for stages, depth in ((1, 6), (2, None)):
+        t = build(gpu, pats, 256, stages, depth)
+        info = gpu.layout_info(t)
+        assert info["filter_mode"] == 2 and info["filter2_bits"] > 0
+        assert same(gpu.scan(t, tx), want)
+
+
 @pytest.mark.parametrize("sigma,lo", [(20, 5), (64, 4), (256, 4), (256, 7)])
 @pytest.mark.parametrize("stages,depth", [(0, None), (1, 6), (2, None)])
 def test_l2_filter_pipeline_random(gpu, monkeypatch, sigma, lo, stages, depth):
