@@ -324,14 +324,6 @@ bool pair_pipeline_enabled()
     return !s || std::strtol(s, nullptr, 10) != 0;
 }
 
-// HEPFAC_PAIR_QUEUE=1: the queue form of the pair filter pass (A/B only; the
-// in-lane form measured 0.5-8% faster: c3, c4 sigma=256, c5 10k).
-bool pair_queue_form()
-{
-    const char* s = std::getenv("HEPFAC_PAIR_QUEUE");
-    return s && std::strtol(s, nullptr, 10) != 0;
-}
-
 // Launches covering fewer starts than this use the one-pass kernel: the
 // two-pass pipeline has ~35 us more fixed cost (a second launch, grid
 // barriers over more warps), and wins only above ~225 MiB (c3 measurements).
@@ -475,9 +467,7 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
             if (im.filter_mode == 4)
                 d->filter_fn = d->kw == 3 ? gpu::pfac_l2_filter_kernel<3> : gpu::pfac_l2_filter_kernel<2>;
             else
-                d->filter_fn = pair_queue_form() ? gpu::pfac_pair_filter_queue_kernel
-                                                 : (v.filter2_bits ? gpu::pfac_pair_filter_kernel<true>
-                                                                   : gpu::pfac_pair_filter_kernel<false>);
+                d->filter_fn = v.filter2_bits ? gpu::pfac_pair_filter_kernel<true> : gpu::pfac_pair_filter_kernel<false>;
         }
         d->walk_kernel = select_cands_kernel(d->grouped, d->identity, d->kw);
         d->walk_smem = size_t(v.key4_words) * 4 + gpu::smem_fixed_bytes(true); // 4-byte-prefix bitmap, queues
@@ -485,11 +475,8 @@ std::shared_ptr<DeviceTrie> make_device_trie(const Trie& t, int device)
         d->walk_blocks_per_sm = std::max(1, d->walk_blocks_per_sm);
         if (im.filter_mode == 4) // the whole shared-memory level, nothing else
             d->filter_smem = size_t(v.filter_l1_words) * 4;
-        else
-            d->filter_smem = size_t(v.filter_words) * 4 +
-                             (im.filter_mode == 3 ? 0
-                                                  : (pair_queue_form() ? gpu::filter_smem_fixed_bytes()
-                                                                       : gpu::filter2_smem_fixed_bytes()));
+        else // the table, plus the pair form's per-warp step staging
+            d->filter_smem = size_t(v.filter_words) * 4 + (im.filter_mode == 3 ? 0 : gpu::pair_smem_fixed_bytes());
         d->filter_blocks_per_sm = occupancy(d->filter_fn, int(gpu::kFThreads), d->filter_smem);
         if (d->filter_blocks_per_sm < 1) fail(HEPFAC_ERR_INTERNAL, "pair filter kernel does not fit an SM");
     }
@@ -882,7 +869,7 @@ uint32_t enqueue_scan(const DeviceTrie& dt, Workspace& ws, const uint8_t* d_text
         if (between) CK(cudaEventRecord(between, ws.stream));
         // the filter pass already tested the L2 bitmap (single + L2; and the
         // pair filter pass, which tests both bits of its survivors)
-        if (dt.filter_mode == 4 || (dt.filter_mode == 2 && !pair_queue_form())) a.trie.filter2_bits = 0;
+        if (dt.filter_mode == 4 || dt.filter_mode == 2) a.trie.filter2_bits = 0;
         a.cand = ws.d_cand;
         a.cand_key = ws.d_cand_key;
         a.cand_cap = ws.cand_cap;

@@ -1,28 +1,24 @@
-// filter_kernel.cuh -- the lean first pass of the pair-filter scan pipeline.
+// filter_kernel.cuh -- the filter passes of the two-pass scan pipeline.
 //
-// Reference semantics: none of its own -- it only discards start offsets that
-// cannot report (a conservative pre-filter of scan.cpp:82-87, where every
-// offset starts a walk).  Every start that survives is walked by the second
-// pass (pfac_scan_kernel<..., CANDS = true>), which produces the records.
+// Reference semantics: none of their own -- they only discard start offsets
+// that cannot report (a conservative pre-filter of scan.cpp:82-87, where
+// every offset starts a walk).  Every start that survives is walked by the
+// second pass (pfac_scan_kernel<..., CANDS = true>), which produces the
+// records.
 //
-// Why a separate kernel: the filter needs ~50 registers, the walk ~120.  In
-// one kernel the walk's register budget caps the SM at 16 warps, and the
-// filter (random shared-memory probes, short dependent chains) is latency
-// bound at 16 warps.  Alone it runs 32 warps per SM.
+// Why separate kernels: a filter needs ~60 registers, the walk ~120.  In one
+// kernel the walk's register budget caps the SM at 16 warps, and the filter
+// (random shared-memory probes, short dependent chains) is latency bound at
+// 16 warps.  Alone it runs 32 warps per SM.
 //
-// Work decomposition (tiles as in scan_kernel.cuh: 8192 starts, round-robin
-// over warps).  A warp takes a tile in steps of kFChunks 512-byte chunks:
-//   - each lane owns 16 consecutive starts of each chunk (one 16-byte LDG,
-//     the 4 overhang bytes from the next lane by SHFL), coalesced 512 B per
-//     warp instruction, the next step prefetched into registers;
-//   - first level: the pair filter (layout.hpp, 8 shared-memory probes per 16
-//     starts), giving a 16-bit mask per chunk;
-//   - second level, batched over the step: the lane's text goes to a per-warp
-//     staging area in shared memory, one warp scan places the candidates in
-//     start order in a queue, and full 32-lane rounds test each candidate's
-//     other role; survivors are appended, still in start order, to the warp's
-//     region of the candidate buffer (u16 tile-relative offsets).
-//   - per tile: survivor count and the slot of its first survivor.
+// Forms: pfac_pair_filter_kernel (pair probes, in-lane
+// second level, optional L2 third level), pfac_l2_filter_kernel (single
+// probe + L2 bitmap for saturated dictionaries), pfac_pack_symbols_kernel +
+// pfac_symbol_filter_kernel (packed symbol keys for sigma <= 4).  All share
+// the tiling (8192-start tiles round-robin over warps, 512-start chunks of 16
+// consecutive starts per lane) and the output: survivors in start order in
+// the warp's region of the candidate buffer (u16 tile offset + first 4 text
+// bytes), a count and slot per tile.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -39,9 +35,6 @@ constexpr uint32_t kFThreads = kFWarps * 32;
 constexpr uint32_t kFChunk = 512;                     // bytes per warp chunk (16 per lane)
 constexpr uint32_t kFChunks = 4;                      // chunks per step
 constexpr uint32_t kFStep = kFChunk * kFChunks;       // 2 KiB
-constexpr uint32_t kFStageStride = kFChunk + 16;      // staged chunk + overhang, 16-aligned
-constexpr uint32_t kFQueue = 512;                     // candidate queue entries (>= one chunk)
-constexpr uint32_t kFWarpSmem = kFChunks * kFStageStride + kFQueue * 2;
 constexpr uint32_t kFTile = 8192;                     // == kTile of scan_kernel.cuh
 
 struct FilterArgs {
@@ -91,183 +84,17 @@ __device__ __forceinline__ uint32_t f_pair_level1(const uint32_t (&w)[5], uint32
     return __brev((m0 << 24) | (m1 << 16)); // start j at bit j
 }
 
-__global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_queue_kernel(const __grid_constant__ FilterArgs a)
-{
-    extern __shared__ __align__(128) uint8_t fsmem[];
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    uint32_t* s_tab = reinterpret_cast<uint32_t*>(fsmem);
-    for (uint32_t i = tid; i < a.table_words; i += kFThreads) s_tab[i] = __ldg(a.table + i);
-    __syncthreads();
-    const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
-    uint8_t* stage = fsmem + size_t(a.table_words) * 4 + warp * kFWarpSmem;
-    uint16_t* q = reinterpret_cast<uint16_t*>(stage + kFChunks * kFStageStride);
-    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-
-    const uint32_t gw = blockIdx.x * kFWarps + warp, W = gridDim.x * kFWarps;
-    const uint32_t shift = a.pair_shift;
-    const uint64_t avail16 = (a.n_avail + 15) & ~15ull;
-    uint16_t* region = a.cand + uint64_t(gw) * a.cand_cap;
-    uint32_t* keys = a.cand_key + uint64_t(gw) * a.cand_cap;
-    // 32-bit cursors: a warp's region never holds more entries than its
-    // starts (< 2^32 unless the text is > 4736 x 4 Gi bytes)
-    const uint32_t cap = uint32_t(min(a.cand_cap, uint64_t(0xFFFFFFFFu)));
-    uint32_t cursor = 0;
-    const uint32_t below = (1u << lane) - 1u;
-    static_assert(kFChunks * kFStageStride <= 2112, "staging offset -> chunk division assumes 4 chunks of 528 B");
-
-    // 16 bytes of lane `lane` of chunk at text offset `at` (zeros past the buffer)
-    auto load = [&](uint64_t at) -> uint4 {
-        const uint64_t p = at + 16u * lane;
-        return p < avail16 ? __ldg(reinterpret_cast<const uint4*>(a.text + p)) : make_uint4(0u, 0u, 0u, 0u);
-    };
-
-    for (uint64_t tile = gw; tile < a.n_tiles; tile += W) {
-        const uint64_t lo = tile * kFTile;
-        const uint32_t slot = cursor;
-        const uint32_t rem = a.start_end > lo ? uint32_t(min(a.start_end - lo, uint64_t(kFTile))) : 0u;
-        const uint32_t steps = (rem + kFStep - 1) / kFStep;
-        uint4 nxt[kFChunks];
-        if (steps) {
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(lo + b * kFChunk);
-        }
-        for (uint32_t s = 0; s < steps; ++s) {
-            const uint64_t sbase = lo + uint64_t(s) * kFStep;
-            uint4 cur[kFChunks];
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
-            if (s + 1 < steps) {
-                const uint64_t nb = sbase + kFStep;
-                if (nb + kFStep <= avail16) { // warp-uniform: the whole next step is in the buffer
-                    const uint4* src = reinterpret_cast<const uint4*>(a.text + nb) + lane;
-#pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = __ldg(src + b * (kFChunk / 16));
-                } else {
-#pragma unroll
-                    for (uint32_t b = 0; b < kFChunks; ++b) nxt[b] = load(nb + b * kFChunk);
-                }
-            }
-            // lane 31's overhang of the last chunk: the first word after the step
-            uint32_t tail = 0;
-            if (lane == 31 && sbase + kFStep < avail16)
-                tail = __ldg(reinterpret_cast<const uint32_t*>(a.text + sbase + kFStep));
-
-            const bool full = (s + 1) * kFStep <= rem; // warp-uniform: every start of the step may report
-            uint32_t mask[kFChunks];
-            uint32_t packed_lo = 0, packed_hi = 0; // survivor counts, 16 bits per chunk
-#pragma unroll
-            for (uint32_t b = 0; b < kFChunks; ++b) {
-                // lane 0 sends the next chunk's first word (lane 31 reads it)
-                const uint32_t send = (lane == 0 && b + 1 < kFChunks) ? cur[(b + 1) % kFChunks].x : cur[b].x;
-                uint32_t ov = __shfl_sync(0xFFFFFFFFu, send, (lane + 1) & 31u);
-                if (lane == 31 && b + 1 == kFChunks) ov = tail;
-                // stage the slice for the second level
-                *reinterpret_cast<uint4*>(stage + b * kFStageStride + 16u * lane) = cur[b];
-                if (lane == 31) *reinterpret_cast<uint32_t*>(stage + b * kFStageStride + kFChunk) = ov;
-                const uint32_t w[5] = {cur[b].x, cur[b].y, cur[b].z, cur[b].w, ov};
-                mask[b] = f_pair_level1(w, tbase, shift);
-                if (!full) {
-                    const int32_t r = int32_t(rem) - int32_t(s * kFStep + b * kFChunk + 16u * lane);
-                    mask[b] &= r >= 16 ? 0xFFFFu : (r > 0 ? (1u << r) - 1u : 0u);
-                }
-                const uint32_t c = uint32_t(__popc(mask[b]));
-                if (b < 2) packed_lo |= c << (16 * b);
-                else packed_hi |= c << (16 * (b - 2));
-            }
-            if (!__any_sync(0xFFFFFFFFu, packed_lo | packed_hi)) continue;
-            __syncwarp(); // staged text visible to the whole warp
-            // one scan per pair of chunks (16-bit fields never carry)
-            uint32_t inc_lo = packed_lo, inc_hi = packed_hi;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t ul = __shfl_up_sync(0xFFFFFFFFu, inc_lo, d);
-                const uint32_t uh = __shfl_up_sync(0xFFFFFFFFu, inc_hi, d);
-                if (lane >= uint32_t(d)) inc_lo += ul, inc_hi += uh;
-            }
-            const uint32_t tot_lo = __shfl_sync(0xFFFFFFFFu, inc_lo, 31);
-            const uint32_t tot_hi = __shfl_sync(0xFFFFFFFFu, inc_hi, 31);
-            uint32_t ex[kFChunks], tot[kFChunks];
-            ex[0] = (inc_lo - packed_lo) & 0xFFFFu, ex[1] = (inc_lo - packed_lo) >> 16;
-            ex[2] = (inc_hi - packed_hi) & 0xFFFFu, ex[3] = (inc_hi - packed_hi) >> 16;
-            tot[0] = tot_lo & 0xFFFFu, tot[1] = tot_lo >> 16, tot[2] = tot_hi & 0xFFFFu, tot[3] = tot_hi >> 16;
-            const uint32_t all = tot[0] + tot[1] + tot[2] + tot[3];
-
-            // Queue chunks [b0, b1) (their candidates fit), then test them in
-            // full rounds and append the survivors to the region.
-            auto run = [&](uint32_t b0, uint32_t b1) {
-                // Queue entries are staging offsets (chunk * 528 + 16 * lane + j),
-                // written two per iteration: lowest bit forward, highest bit
-                // backward.
-                uint32_t base = 0;
-#pragma unroll
-                for (uint32_t b = 0; b < kFChunks; ++b) {
-                    if (b < b0 || b >= b1) continue;
-                    uint32_t at = base + ex[b], back = at + __popc(mask[b]) - 1;
-                    const uint32_t first = b * kFStageStride + 16u * lane;
-                    for (uint32_t m = mask[b]; m;) {
-                        const uint32_t lo = __ffs(m) - 1, hi = 31 - __clz(m);
-                        q[at++] = uint16_t(first + lo);
-                        if (hi != lo) q[back--] = uint16_t(first + hi);
-                        m &= ~((1u << lo) | (1u << hi));
-                    }
-                    base += tot[b];
-                }
-                __syncwarp();
-                for (uint32_t r0 = 0; r0 < base; r0 += 32) {
-                    const uint32_t e = r0 + lane;
-                    uint32_t so = 0, y = 0;
-                    bool keep = false;
-                    if (e < base) {
-                        so = q[e]; // staging offset of the start
-                        const uint32_t sa = stage_s + so;
-                        uint32_t lo4, hi4;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo4) : "r"(sa & ~3u));
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi4) : "r"((sa & ~3u) + 4));
-                        y = __funnelshift_r(lo4, hi4, 8 * (sa & 3u)); // bytes off..off+3
-                        const bool odd = so & 1u; // chunk and lane offsets are even
-                        const uint32_t mid = odd ? (y >> 8) : y;
-                        const uint32_t amt = odd ? y : (y >> 24);
-                        const uint32_t word = f_lds(tbase + (((mid * kPairMul) >> shift) << 2));
-                        keep = int32_t(word << (amt & 31u)) < 0;
-                    }
-                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
-                    if (keep) {
-                        const uint32_t at = cursor + __popc(bal & below);
-                        if (at < cap) {
-                            const uint32_t c = (so * 125u) >> 16; // so / 528 for every valid so < 2112
-                            region[at] = uint16_t(s * kFStep + so - 16u * c);
-                            keys[at] = y;
-                        }
-                    }
-                    cursor += __popc(bal);
-                }
-                __syncwarp(); // queue reads done before the next writes
-            };
-            if (all <= kFQueue) {
-                run(0, kFChunks);
-            } else {
-                for (uint32_t b = 0; b < kFChunks; ++b)
-                    if (tot[b]) run(b, b + 1);
-            }
-        }
-        if (lane == 0) {
-            a.tile_ccount[tile] = cursor - slot;
-            a.tile_cslot[tile] = uint32_t(slot);
-        }
-    }
-    if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
-}
-
-// ---- pair form, in-lane second level ---------------------------------------------
+// ---- pair form -------------------------------------------------------------------
 //
-// Same tiles, loads, first level and candidate output as the queue form
-// above, with the second level done by each lane on its own first-level
-// survivors, reading their bytes back from the step staged contiguously in
-// shared memory (the step's 2 KiB + the 4 bytes after it).  The queue form
-// spends ~36% of its instructions building the queue and running full-warp
-// rounds on it; here a step costs max-over-lanes(survivors) iterations of a
-// ~20-instruction loop (about 6 at c3's 3.7% first-level pass rate), and the
-// final survivors (~0.1%) are placed in start order by one ballot per chunk.
+// Per 2 KiB step a lane loads its 4 slices (16 B each, coalesced), the step
+// is staged contiguously in shared memory, and the first level (8 pair
+// probes per slice) gives 16 bits per slice.  The second level is done by
+// each lane on its own first-level survivors, reading their bytes back from
+// the staged step: a step costs max-over-lanes(survivors) iterations of a
+// ~27-instruction loop.  (A queue form that redistributed survivors to full
+// 32-lane rounds spent 36% of the pass building the queue and was measured
+// 0.5-8% slower: c3, c4 sigma=256, c5 10k.)  Final survivors (~0.1%) are
+// placed in start order by one ballot per chunk.
 constexpr uint32_t kPStage = kFStep + 16;             // staged step + the word after it
 constexpr uint32_t kPWarpSmem = kPStage;
 
@@ -329,7 +156,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             for (uint32_t b = 0; b < kFChunks; ++b) cur[b] = nxt[b];
             // the next step's loads: issued after this step's second level, so
             // their registers are not live across it (+2% at c3 against issuing
-            // them here; HFB_LATE_PREFETCH=0 restores that)
+            // them one step ahead at the top of the step)
             auto prefetch = [&]() {
                 if (s + 1 < steps) {
                     const uint64_t nb = sbase + kFStep;
@@ -343,9 +170,6 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                     }
                 }
             };
-#if defined(HFB_LATE_PREFETCH) && !HFB_LATE_PREFETCH
-            prefetch();
-#endif
             // the 4 bytes after the step (8 with the third level: its keys
             // reach 8 bytes past a start)
             uint2 tail = make_uint2(0u, 0u);
@@ -381,9 +205,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                 else m23 |= m << 16;
             }
             if (!__any_sync(0xFFFFFFFFu, m01 | m23)) {
-#if !defined(HFB_LATE_PREFETCH) || HFB_LATE_PREFETCH
                 prefetch();
-#endif
                 continue;
             }
 
@@ -464,9 +286,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
                 m01 &= ~uint32_t(fail);
                 m23 &= ~uint32_t(fail >> 32);
             }
-#if !defined(HFB_LATE_PREFETCH) || HFB_LATE_PREFETCH
             prefetch();
-#endif
             if (!__any_sync(0xFFFFFFFFu, m01 | m23)) continue;
             const uint32_t n01 = __popc(m01), n23 = __popc(m23);
             // final survivors in start order (chunk, lane, position).  Common
@@ -688,8 +508,7 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_l2_filter_kernel(const __gr
     if (lane == 0 && cursor > cap) atomicMax(a.cand_need, (unsigned long long)cursor);
 }
 
-constexpr uint32_t filter_smem_fixed_bytes() { return kFWarps * kFWarpSmem; }
-constexpr uint32_t filter2_smem_fixed_bytes() { return kFWarps * kPWarpSmem; }
+constexpr uint32_t pair_smem_fixed_bytes() { return kFWarps * kPWarpSmem; }
 
 // ---- symbol-key form (small alphabets) ------------------------------------------
 

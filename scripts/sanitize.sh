@@ -5,7 +5,7 @@
 set -u
 out=gpurun_out/sanitize
 mkdir -p $out
-cases="${CASES:-fused_pair fused_single fused_dna two_pass_queue two_pass_inlane two_pass_pair_l2 two_pass_l2 symbol streamed session}"
+cases="${CASES:-fused_pair fused_single fused_dna two_pass_pair two_pass_pair_l2 two_pass_l2 symbol streamed session}"
 for tool in ${TOOLS:-memcheck synccheck racecheck initcheck}; do
     for c in $cases; do
         timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \

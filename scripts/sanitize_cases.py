@@ -67,10 +67,8 @@ CASES = {
     "fused_pair": lambda: run("fused_pair", 256, 300, 4, 20, 1 << 20),
     "fused_single": lambda: run("fused_single", 20, 300, 6, 20, 1 << 20, env={"HEPFAC_FILTER_MODE": "single"}),
     "fused_dna": lambda: run("fused_dna", 4, 300, 8, 20, 1 << 20, stages=2),
-    "two_pass_queue": lambda: run("two_pass_queue", 256, 300, 4, 20, 1 << 20, depth=4,
-                                  env={"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_QUEUE": "1"}),
-    "two_pass_inlane": lambda: run("two_pass_inlane", 256, 300, 4, 20, 1 << 20,
-                                   env={"HEPFAC_PIPELINE_MIN_MIB": "0"}),
+    "two_pass_pair": lambda: run("two_pass_pair", 256, 300, 4, 20, 1 << 20, depth=4,
+                                 env={"HEPFAC_PIPELINE_MIN_MIB": "0"}),
     "two_pass_pair_l2": lambda: run("two_pass_pair_l2", 256, 30000, 4, 24, 1 << 16,
                                     env={"HEPFAC_PIPELINE_MIN_MIB": "0"}),
     "two_pass_l2": lambda: run("two_pass_l2", 256, 300, 4, 20, 1 << 20, env={"HEPFAC_PIPELINE_MIN_MIB": "0",

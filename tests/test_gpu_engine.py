@@ -161,12 +161,12 @@ def test_output_invariant_across_engine_configurations(gpu, monkeypatch):
     # The reference asserts byte-identical output for every worker count and
     # chunk size (acceptance.cpp:274-332, test_scan.cpp:43-56).  Here the
     # same list must come out of every engine configuration: one-pass fused
-    # kernel or two-pass pipeline (queue or in-lane filter pass), 1 MiB or
+    # kernel or two-pass pipeline (or pair tries kept on the fused kernel), 1 MiB or
     # 64 MiB chunks, one device or three shards, and any scan config.
     pats, tx = dense_instance(21, mib=3, every=509)
     t = build(gpu, pats, 256, 1, 5)
     want = oracle.naive_find_all(tx, pats)
-    combos = [{}, {"HEPFAC_PIPELINE_MIN_MIB": "0"}, {"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_QUEUE": "1"},
+    combos = [{}, {"HEPFAC_PIPELINE_MIN_MIB": "0"}, {"HEPFAC_PIPELINE_MIN_MIB": "0", "HEPFAC_PAIR_PIPELINE": "0"},
               {"HEPFAC_CHUNK_MIB": "1"}, {"HEPFAC_CHUNK_MIB": "1", "HEPFAC_PIPELINE_MIN_MIB": "0"},
               {"HEPFAC_DEVICES": "0,0,0"}, {"HEPFAC_DEVICES": "0,0", "HEPFAC_PIPELINE_MIN_MIB": "0"}]
     keys = {k for c in combos for k in c}
