@@ -1311,6 +1311,9 @@ std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t
     const uint64_t reach = t.device_image(devs[0])->reach;
     if (reach == UINT64_MAX) return scan_one(t, text, bytes, bytes, 0, devs[0]); // cyclic: no halo bound
     const uint64_t halo = reach ? reach - 1 : 0;
+    // (declared before the jobs: on an error the jobs' workspaces synchronize
+    // their streams before the list their copies target is freed)
+    auto out = std::make_unique<MatchList>();
     std::vector<ShardJob> jobs(G);
     std::vector<std::exception_ptr> errs(G);
     auto parallel = [&](auto&& fn) {
@@ -1334,7 +1337,6 @@ std::unique_ptr<MatchList> gpu_scan(const Trie& t, const uint8_t* text, uint64_t
     });
     std::vector<uint64_t> prefix(G + 1, 0); // the count exchange: exclusive scan of shard totals
     for (uint64_t g = 0; g < G; ++g) prefix[g + 1] = prefix[g] + jobs[g].total;
-    auto out = std::make_unique<MatchList>();
     out->allocate(size_t(prefix[G]));
     parallel([&](uint64_t g) {
         if (!jobs[g].total) return;
