@@ -39,7 +39,7 @@ prof c2_pack 'pfac_pack_dna' 1 _ZN3hfb3gpu20pfac_pack_dna_kernelILb1EEEvPKhmPKtj
 prof c5m_l2 pfac_l2_filter_kernel 1 _ZN3hfb3gpu21pfac_l2_filter_kernelILi3EEEvNS0_10FilterArgsE --config c5 --count 1000000 --bytes-per-gpu $G
 if [ "${PROBE:-1}" = 1 ]; then
 timeout 2400 python scripts/probe.py --check --full-check --iters 5 \
-    --configs c1,c2,c3,c4:2,c4:4,c4:20,c4:64,c4:128,c4:256,c5:1000,c5:10000,c5:100000,c5:1000000 \
+    --configs ${PROBE_CONFIGS:-c1,c2,c3,c4:2,c4:4,c4:20,c4:64,c4:128,c4:256,c5:1000,c5:10000,c5:100000,c5:1000000} \
     > $out/probe_configs.jsonl 2>> $out/bench.err
 fi
 echo done
