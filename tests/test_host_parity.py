@@ -307,3 +307,26 @@ def test_million_pattern_compile_time(lib):
     t3 = time.perf_counter()
     assert st.nodes_before == 16041198 and s2.node_count() == 13192775 and halo == 31
     assert t3 - t0 < 90, (t1 - t0, t2 - t1, t3 - t2)
+
+
+def test_workload_text_ranges_are_slices_of_one_text(lib):
+    # bench.py gives every rank exactly its global bytes [lo, lo + n) of one
+    # text (16 MiB blocks, each generated on its own), so shard halos are the
+    # next rank's real bytes and a one-rank scan of the whole text is the
+    # check (bench.py --check).  Ranges across block seams equal slices of
+    # the whole; plants land in every block; config 4 refuses to make a text
+    # before the library has generated its pattern set.
+    import numpy as np
+    import pytest
+    w = workloads.config("c1")
+    whole = w.make_text(40 << 20)
+    for lo, n in ((0, 1), (5, 1000), ((16 << 20) - 7, 100), ((16 << 20) - 3, (17 << 20) + 11), (39 << 20, 1 << 20)):
+        assert np.array_equal(w.make_text(n, lo=lo), whole[lo:lo + n])
+    for b in range(2):
+        blk = whole[b * (16 << 20):(b + 1) * (16 << 20)]
+        assert sum(blk.tobytes().count(p) for p in w.patterns[:50]) > 0
+    w4 = workloads.config("c4", sigma=4)
+    with pytest.raises(ValueError):
+        w4.make_text(1024)
+    workloads.build_trie(lib, w4, "full")
+    assert w4.make_text(1024).size == 1024
