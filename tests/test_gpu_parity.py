@@ -640,3 +640,25 @@ def test_direct_index_small_alphabet(gpu, monkeypatch, alphabet, stages, depth):
     t2 = gpu.build_trie(gpu.patterns(pats, a))
     assert gpu.layout_info(t2)["filter_mode"] != 5
     assert same(gpu.scan(t2, tx), want)
+
+
+def test_direct_index_tiny_and_ragged_texts(gpu):
+    # The direct-index path at the text end: every text length 0..96 and a
+    # few ragged ones past the pack pass's 32-byte blocks, with occurrences
+    # that end exactly at the last byte, overhang it, or contain a byte
+    # outside the alphabet.
+    rng = np.random.default_rng(2024)
+    a = gpu.alphabet("ACGT")
+    syms = np.frombuffer(b"ACGT", dtype=np.uint8)
+    pats = sorted(set(pattern_set(rng, syms, 300, 8, 32)) | {b"ACGTACGT", b"ACGTACGTA", b"ACGTACGTAC"})
+    t = gpu.build_trie(gpu.patterns(pats, a))
+    assert gpu.layout_info(t)["filter_mode"] == 5
+    for n in list(range(0, 97)) + [127, 128, 129, 4095, 4097, 65535]:
+        tx = text(rng, syms, n)
+        if n >= 10:
+            plant(tx, b"ACGTACGTAC", n - 10)  # ends at the last byte
+        if n >= 9:
+            plant(tx, pats[n % len(pats)][: 9], n - 9)
+        if n > 40 and n % 3 == 0:
+            tx[n // 2] = ord("N")
+        assert same(gpu.scan(t, tx), oracle.naive_find_all(tx, pats)), n
