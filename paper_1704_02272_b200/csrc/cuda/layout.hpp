@@ -120,19 +120,25 @@ HFB_HD uint32_t filter2_slot(uint32_t x, uint32_t bits) { return filter2_hash(x)
 constexpr uint32_t kJumpWords = 8;
 // Inline pattern lists: when at most kJumpExtEntries patterns start with a
 // slot's key (flags bit 2 = kJumpInline, the count in bits 3-4), the parallel
-// extension table (tables up to 2^kMaxJumpExtBits slots) holds each as {id,
+// extension table (tables up to 2^kMaxJumpExtBits slots: 256 MiB) holds each as {id,
 // len, 24 pattern bytes [inline_skip, +24), zero padded}, in (length, id) order.
 // They are every record a start with that key can emit (the trie accepts
 // exactly its dictionary), so instead of walking the subtree (or reading the
 // terminal and bucket at the depth limit) the start verifies them against the
-// text with one extension load.
+// text with one extension load.  The cap was 2^19 slots (L2-sized) until c5 at
+// 1M patterns (2^21 slots) was measured: its stage-2 DAG walks are HBM round
+// trips per byte, and the two dependent loads of slot + list are cheaper
+// (469 -> 518 GB/s of text).
 constexpr uint32_t kJumpInline = 4u;
 constexpr uint32_t kJumpInlineShift = 3u;
 constexpr uint32_t kJumpExtEntries = 2;
 constexpr uint32_t kJumpExtEntryWords = 8;
 constexpr uint32_t kJumpExtBytes = 4 * (kJumpExtEntryWords - 2);
 constexpr uint32_t kJumpExtWords = kJumpExtEntries * kJumpExtEntryWords;
-constexpr uint32_t kMaxJumpExtBits = 19;
+#ifndef HFB_MAX_JUMP_EXT_BITS
+#define HFB_MAX_JUMP_EXT_BITS 22
+#endif
+constexpr uint32_t kMaxJumpExtBits = HFB_MAX_JUMP_EXT_BITS;
 HFB_HD uint32_t jump_slot(uint32_t key32, uint32_t bits) { return filter2_hash(key32) >> (32 - bits); }
 HFB_HD uint32_t jump_slot2(uint32_t key32, uint32_t bits)
 {

@@ -76,7 +76,7 @@ uint32_t ceil_log2(uint64_t x)
 // are the key; a slot with word 2 == kNoId is empty.  Grows until every key
 // places (load <= 1/2 to start).  `lists[i]` (optional) names every pattern
 // with entry i's k-prefix when there are at most kJumpExtEntries of them
-// (flags bit 2, see inline_lists); while the table stays L2-sized those go to
+// (flags bit 2, see inline_lists); up to 2^kMaxJumpExtBits slots those go to
 // the slot's extension (layout.hpp), otherwise bit 2 is cleared.
 using JumpEntry = std::array<uint32_t, kJumpWords>;
 using InlineList = std::array<uint32_t, kJumpExtEntries>;
