@@ -90,8 +90,8 @@ __device__ __forceinline__ uint32_t f_pair_level1(const uint32_t (&w)[5], uint32
 // is staged contiguously in shared memory, and the first level (8 pair
 // probes per slice) gives 16 bits per slice.  The second level is done by
 // each lane on its own first-level survivors, reading their bytes back from
-// the staged step: a step costs max-over-lanes(survivors) iterations of a
-// ~27-instruction loop.  (A queue form that redistributed survivors to full
+// the staged step: one loop over the lane's 64 starts, so a step costs
+// max-over-lanes(survivors) iterations of a ~32-instruction loop.  (A queue form that redistributed survivors to full
 // 32-lane rounds spent 36% of the pass building the queue and was measured
 // 0.5-8% slower: c3, c4 sigma=256, c5 10k.)  Final survivors (~0.1%) are
 // placed in start order by one ballot per chunk.
@@ -212,40 +212,73 @@ __global__ void __launch_bounds__(kFThreads, 1) pfac_pair_filter_kernel(const __
             // second level, in-lane: the other role of each first-level
             // survivor, highest bit first (bit j of a word = chunk j/16,
             // position j%16 of the lane's slice; m01: chunks 0-1, m23: 2-3).
-            // One loop over both words -- a step costs max over lanes of the
-            // lane's survivors -- walking m01 first, then m23: the switch is a
-            // rare branch instead of a select on every variable.  Failing bits
-            // are cleared.
+            // Failing bits are cleared.
             {
                 // loop constants kept opaque, so they stay in registers
                 uint32_t k_one, k_mul, k_shift;
                 asm("mov.u32 %0, 1;" : "=r"(k_one));
                 asm("mov.u32 %0, %1;" : "=r"(k_mul) : "n"(kPairMul));
                 asm("mov.u32 %0, %1;" : "=r"(k_shift) : "r"(shift));
+                // one second-level test of bit j (0..31) of the mask whose
+                // chunk pair starts at `base`; returns bit j if it fails
+                auto test = [&](uint32_t base, uint32_t j, uint32_t bit, uint32_t& fail) {
+                    const uint32_t at = base + j + (j >> 4) * (kFChunk - 16u); // + chunk * 512 + position
+                    uint32_t w0, w1, t;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(at & ~3u));
+                    asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w1) : "r"(at & ~3u));
+                    asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(t) : "r"(w0), "r"(w1), "r"(at)); // p0 p1 p2 p3
+                    // odd starts passed role B and test A: H(p1 p2 p3), bit p0;
+                    // even ones test B: H(p0 p1 p2), bit p3.  sh = 8 for odd j:
+                    // mid = t >> sh, and the amount t >> (24 + sh) mod 32.
+                    const uint32_t sh = (j << 3) & 8u;
+                    const uint32_t mid = t >> sh, amt = __funnelshift_r(t, 0u, sh + 24u);
+                    const uint32_t word = f_lds(tbase + (((mid * k_mul) >> k_shift) << 2));
+                    // fail |= bit unless the tested bit (now the sign) is set:
+                    // one arithmetic shift and one LOP3 instead of a compare,
+                    // a select and an OR
+                    uint32_t sgn;
+                    asm("shr.s32 %0, %1, 31;" : "=r"(sgn) : "r"(__funnelshift_l(0u, word, amt)));
+                    asm("lop3.b32 %0, %1, %2, %3, 0xF4;" : "=r"(fail) : "r"(fail), "r"(bit), "r"(sgn)); // fail | (bit & ~sgn)
+                };
+                const uint32_t base01 = stage_s + 16u * lane;
                 uint32_t fail01 = 0, fail23 = 0;
-#pragma unroll
-                for (uint32_t half = 0; half < 2; ++half) {
-                    const uint32_t base = stage_s + 16u * lane + half * 2u * kFChunk;
-                    uint32_t fail = 0;
-                    for (uint32_t x = half ? m23 : m01; x;) {
+                if constexpr (!L2) {
+                    // one loop over both words (m23 first): a step costs the
+                    // maximum over lanes of the lane's survivors, not the sum of
+                    // the two words' maxima.  When the current word runs out the
+                    // other one takes its place (predicated, no branch): 32
+                    // instructions per iteration against 24, for ~6.1 iterations
+                    // per step against ~7.8 at c3 (+0.7-2.7% on c3, c4 sigma=64/256,
+                    // c5 1k/10k).  The third-level instantiation keeps two loops
+                    // (c5 100k: +4.5% with two, +0.6% with one).
+                    uint32_t x = m23, fail = 0, f23 = 0, base = base01 + 2u * kFChunk;
+                    bool second = false;
+                    if (!x) x = m01, second = true, base = base01;
+                    while (x) {
                         uint32_t j;
                         asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(x)); // highest set bit
                         const uint32_t bit = k_one << j;
                         x ^= bit;
-                        const uint32_t at = base + j + (j >> 4) * (kFChunk - 16u); // + chunk * 512 + position
-                        uint32_t w0, w1, t;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(at & ~3u));
-                        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w1) : "r"(at & ~3u));
-                        asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(t) : "r"(w0), "r"(w1), "r"(at)); // p0 p1 p2 p3
-                        // odd starts passed role B and test A: H(p1 p2 p3), bit p0;
-                        // even ones test B: H(p0 p1 p2), bit p3
-                        const bool odd = j & 1u;
-                        const uint32_t mid = odd ? t >> 8 : t, amt = odd ? t : t >> 24;
-                        const uint32_t word = f_lds(tbase + (((mid * k_mul) >> k_shift) << 2));
-                        if (int32_t(__funnelshift_l(0u, word, amt)) >= 0) fail |= bit;
+                        test(base, j, bit, fail);
+                        if (!x && !second) x = m01, f23 = fail, fail = 0, base = base01, second = true;
                     }
-                    if (half) fail23 = fail;
-                    else fail01 = fail;
+                    fail23 = second ? f23 : fail;
+                    fail01 = second ? fail : 0u;
+                } else {
+#pragma unroll
+                    for (uint32_t half = 0; half < 2; ++half) {
+                        const uint32_t base = base01 + half * 2u * kFChunk;
+                        uint32_t fail = 0;
+                        for (uint32_t x = half ? m23 : m01; x;) {
+                            uint32_t j;
+                            asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(x)); // highest set bit
+                            const uint32_t bit = k_one << j;
+                            x ^= bit;
+                            test(base, j, bit, fail);
+                        }
+                        if (half) fail23 = fail;
+                        else fail01 = fail;
+                    }
                 }
                 m01 &= ~fail01;
                 m23 &= ~fail23;
