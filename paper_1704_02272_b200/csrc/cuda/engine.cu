@@ -1005,16 +1005,21 @@ unsigned copy_threads()
 
 // Persistent helper threads for par_memcpy (spawning threads per 64 MiB
 // chunk would cost ~10% of a streamed scan).  Concurrent callers share them.
+// A streamed scan hands them one staging piece (2-16 MiB) at a time, so a
+// helper that finishes a task spins for a while (HEPFAC_COPY_SPIN_US, default
+// 2000: longer than a 16 MiB piece's DMA, which is what the caller waits on
+// between pieces once the ring is full) before it sleeps on the condition
+// variable, and the caller spins on its batch the same way.  A sleeping
+// thread's wake-up per piece cost small pageable scans most (Gbps through
+// hepfac_scan, c3 text, sleeping / spinning helpers, scripts/e2e_sizes.py):
+// 16 MiB 153 / 182, 64 MiB 217 / 295, 256 MiB 305 / 372, 1 GiB 360-400 / 419
+// against 319 / 388 / 430 / 440 from pinned text.
 class CopyPool {
 public:
     // Runs fn(0..parts-1): the caller runs part 0, helpers the rest (the
     // pool grows to parts - 1 helpers on first need).
     void run(unsigned parts, const std::function<void(unsigned)>& fn)
     {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            while (workers_.size() + 1 < parts) workers_.emplace_back([this] { loop(); });
-        }
         struct Batch {
             std::atomic<unsigned> left;
             std::mutex mu;
@@ -1023,38 +1028,75 @@ public:
         batch.left = parts - 1;
         {
             std::lock_guard<std::mutex> lk(mu_);
+            while (workers_.size() + 1 < parts) workers_.emplace_back([this] { loop(); });
             for (unsigned i = 1; i < parts; ++i)
                 tasks_.push_back([&batch, &fn, i] {
                     fn(i);
-                    if (batch.left.fetch_sub(1) == 1) {
-                        std::lock_guard<std::mutex> g(batch.mu);
-                        batch.cv.notify_all();
-                    }
+                    // decrement under the batch mutex: the caller takes it
+                    // before returning, so `batch` (its stack) outlives this
+                    std::lock_guard<std::mutex> g(batch.mu);
+                    if (batch.left.fetch_sub(1, std::memory_order_acq_rel) == 1) batch.cv.notify_all();
                 });
+            queued_.fetch_add(parts - 1, std::memory_order_release);
+            if (sleepers_) cv_.notify_all();
         }
-        cv_.notify_all();
         fn(0);
-        std::unique_lock<std::mutex> lk(batch.mu);
-        batch.cv.wait(lk, [&] { return batch.left.load() == 0; });
+        const auto t0 = std::chrono::steady_clock::now();
+        while (batch.left.load(std::memory_order_acquire) != 0 && std::chrono::steady_clock::now() - t0 <= spin_)
+            relax();
+        std::unique_lock<std::mutex> lk(batch.mu); // also waits out the last helper's critical section
+        batch.cv.wait(lk, [&] { return batch.left.load(std::memory_order_acquire) == 0; });
     }
 
 private:
+    static void relax()
+    {
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#else
+        std::this_thread::yield();
+#endif
+    }
+    static std::chrono::microseconds spin_us()
+    {
+        long v = 2000;
+        if (const char* s = std::getenv("HEPFAC_COPY_SPIN_US")) v = std::clamp(std::strtol(s, nullptr, 10), 0L, 100000L);
+        return std::chrono::microseconds(v);
+    }
     void loop()
     {
         for (;;) {
             std::function<void()> task;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return !tasks_.empty(); });
-                task = std::move(tasks_.front());
-                tasks_.pop_front();
+            const auto t0 = std::chrono::steady_clock::now();
+            while (!task) {
+                if (queued_.load(std::memory_order_acquire) != 0) {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    if (!tasks_.empty()) {
+                        task = std::move(tasks_.front());
+                        tasks_.pop_front();
+                        queued_.fetch_sub(1, std::memory_order_relaxed);
+                    }
+                } else if (std::chrono::steady_clock::now() - t0 > spin_) {
+                    std::unique_lock<std::mutex> lk(mu_);
+                    ++sleepers_;
+                    cv_.wait(lk, [&] { return !tasks_.empty(); });
+                    --sleepers_;
+                    task = std::move(tasks_.front());
+                    tasks_.pop_front();
+                    queued_.fetch_sub(1, std::memory_order_relaxed);
+                } else {
+                    relax();
+                }
             }
             task();
         }
     }
+    const std::chrono::microseconds spin_ = spin_us();
     std::mutex mu_;
     std::condition_variable cv_;
     std::deque<std::function<void()>> tasks_;
+    std::atomic<unsigned> queued_{0};
+    unsigned sleepers_ = 0; // guarded by mu_
     std::vector<std::thread> workers_;
 };
 

@@ -87,6 +87,26 @@ def test_pageable_pinned_and_device_inputs_agree(gpu, monkeypatch, two_pass):
     assert same(gpu._list(h), want)
 
 
+def test_many_small_pageable_scans(gpu, monkeypatch):
+    # Each staging piece is one batch of the host copy pool (helpers spin
+    # between pieces, then sleep); hundreds of short scans with 1 MiB pieces
+    # exercise the hand-off between the caller and the helpers.
+    monkeypatch.setenv("HEPFAC_STAGE_MIB", "1")
+    rng = np.random.default_rng(31)
+    syms = np.arange(256, dtype=np.uint8)
+    pats = pattern_set(rng, syms, 300, 4, 16)
+    t = build(gpu, pats, 256, 1)
+    tx = text(rng, syms, (5 << 20) + 13)
+    for i in range(0, tx.size - 64, 4099):
+        plant(tx, pats[i % len(pats)], i)
+    want = oracle.naive_find_all(tx, pats)
+    for k in range(300):
+        n = tx.size - 4096 * (k % 7)
+        got = gpu.scan(t, tx[:n])
+        assert gpu.last_scan_stats()["staged"] == 1
+        assert same(got, want[want["start"] + want["length"] <= n])
+
+
 def test_match_list_growth_and_reuse(gpu, monkeypatch):
     # The host list is reserved from the first chunks' record rate and grown
     # when a later chunk outruns it; repeated scans reuse pooled pinned blocks.
