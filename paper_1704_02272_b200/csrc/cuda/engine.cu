@@ -990,9 +990,11 @@ uint64_t stream_chunk_bytes()
 
 // Host-to-host copy into a pinned staging buffer on several threads: one
 // memcpy thread moves ~10 GB/s, the PCIe Gen5 H2D it feeds ~55 GB/s.
-// HEPFAC_COPY_THREADS overrides the count (default: 3/4 of the host threads,
-// at most 12; on a 16-thread B200 host 8-12 threads reach ~43 GB/s, more do
-// not help).
+// HEPFAC_COPY_THREADS overrides the count (default: half the host threads, at
+// most 8.  On the 16-thread B200 host, with the helpers spinning between
+// pieces, 8 beat 12 through hepfac_scan from 1 GiB of pageable text: c2 391-393
+// against 360-384 Gbps, c3 421 against 407-419 -- spinning helpers on every
+// core starve the driver and the caller).
 unsigned copy_threads()
 {
     if (const char* s = std::getenv("HEPFAC_COPY_THREADS")) {
@@ -1000,7 +1002,7 @@ unsigned copy_threads()
         if (v >= 1) return unsigned(std::min<long>(v, 64));
     }
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    return std::clamp(hw * 3 / 4, 1u, 12u);
+    return std::clamp(hw / 2, 1u, 8u);
 }
 
 // Persistent helper threads for par_memcpy (spawning threads per 64 MiB
