@@ -58,6 +58,24 @@ void parallel_slices(size_t n, size_t grain, Fn&& fn)
     for (auto& th : pool) th.join();
 }
 
+// Vector whose resize(n) leaves the new elements uninitialised, so a large
+// trie's cells are first touched (and paged in) by the threads that fill them.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept { ::new (static_cast<void*>(p)) U; }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
+};
+using CellVector = std::vector<uint32_t, DefaultInitAlloc<uint32_t>>;
+
 // ---------------------------------------------------------------------------
 // Alphabet: dense byte <-> symbol map (reference alphabet.hpp:13-47).
 class Alphabet {
@@ -126,7 +144,7 @@ public:
     Alphabet alphabet;
     uint32_t words;
     uint32_t node_count = 0;
-    std::vector<uint32_t> cells; // node i: cells[i*stride .. +words) bitmap, then offset word
+    CellVector cells; // node i: cells[i*stride .. +words) bitmap, then offset word
     std::vector<std::string> patterns;
     uint32_t min_len = 0, max_len = 0;
     Stage stage = Stage::None;

@@ -99,7 +99,7 @@ std::unique_ptr<Trie> decode_htri(const uint8_t* data, size_t size)
 
     const size_t ncells = size_t(nodes) * (words + 1);
     r.need(ncells * 4);
-    std::vector<uint32_t> cells(ncells);
+    CellVector cells(ncells);
     for (auto& c : cells) c = r.u32();
 
     const uint32_t count = r.u32();

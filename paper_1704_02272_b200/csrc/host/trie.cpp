@@ -15,6 +15,7 @@
 // level from the symbol-sorted pattern list (no pointer graph, no queue),
 // and rewrites operate on a flat CSR graph.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <numeric>
 #include <thread>
@@ -135,7 +136,7 @@ std::unique_ptr<Trie> build_trie(const PatternSet& set)
 
     auto t = std::make_unique<Trie>(a);
     const uint32_t stride = t->stride();
-    std::vector<uint32_t>& cells = t->cells;
+    CellVector& cells = t->cells;
     cells.assign(stride, 0); // root
     uint64_t nodes = 1;
 
@@ -220,7 +221,18 @@ Graph graph_of(const Trie& t)
     return g;
 }
 
-// Breadth-first first-reference emission (the reference's TrieAssembler rule).
+// Breadth-first first-reference emission (the reference's TrieAssembler rule,
+// trie.cpp:133-217): slots are appended in BFS order; a multi-child node's
+// children take one consecutive run, where an already-placed child becomes a
+// copy slot; a single child is linked to its primary slot; every node's
+// primary slot is its first reference in BFS order.
+//
+// Here the queue is processed a whole BFS level at a time, on all host
+// threads.  The slots of level l+1 are created by the references of level
+// l's slots, in (slot, edge) order, so "first reference" is the minimum
+// reference index among a child's references in the level (an atomic
+// minimum), and a prefix sum over the heads numbers the new slots.  The
+// result is identical to the one-slot-at-a-time queue.
 // `bucket_src` (optional) maps source node -> pattern ids; keys are remapped to
 // the emitted primary slots.
 std::unique_ptr<Trie> emit(const Graph& g, const Trie& like, Stage stage,
@@ -228,56 +240,109 @@ std::unique_ptr<Trie> emit(const Graph& g, const Trie& like, Stage stage,
                            const std::vector<std::pair<uint32_t, std::vector<uint32_t>>>* bucket_src)
 {
     constexpr uint32_t kUnplaced = Trie::kNone;
+    constexpr size_t kGrain = 1 << 14;
     std::vector<uint32_t> slot_of_node(g.size(), kUnplaced); // primary slot per graph node
-    std::vector<uint32_t> node_of_slot;
-    std::vector<uint8_t> copy_slot;
-    std::vector<uint32_t> child_base;
+    // minimum reference index of each node in the level that places it (a
+    // node is referenced while unplaced in exactly one level: its first
+    // reference places it)
+    std::vector<uint32_t> first_ref(g.size(), kUnplaced);
+    std::vector<uint32_t> node_of_slot{0};
+    std::vector<uint8_t> copy_slot{0};
+    std::vector<uint32_t> child_base{0};
+    slot_of_node[0] = 0;
+    // every slot but the root is made by one reference (edge) of a slot
+    const size_t max_slots = std::min<size_t>(size_t(Trie::kMaxNodes), g.dst.size() + 1);
+    node_of_slot.reserve(max_slots);
+    copy_slot.reserve(max_slots);
+    child_base.reserve(max_slots);
 
-    auto new_slot = [&](uint32_t u, bool copy) {
-        uint32_t s = uint32_t(node_of_slot.size());
-        if (s >= Trie::kMaxNodes) fail(HEPFAC_ERR_INTERNAL, "trie exceeds 2^31-1 nodes");
-        node_of_slot.push_back(u);
-        copy_slot.push_back(copy ? 1 : 0);
-        child_base.push_back(0);
-        if (!copy) slot_of_node[u] = s;
-        return s;
-    };
-
-    new_slot(0, false);
-    for (size_t head = 0; head < node_of_slot.size(); ++head) {
-        if (copy_slot[head]) continue; // copies are never expanded
-        const uint32_t u = node_of_slot[head];
-        const uint32_t deg = g.degree[u];
-        if (deg == 0) continue;
-        if (deg == 1) {
-            const uint32_t c = g.only_child(u);
-            if (slot_of_node[c] == kUnplaced) new_slot(c, false);
-            child_base[head] = slot_of_node[c];
-            continue;
-        }
-        const uint32_t run = uint32_t(node_of_slot.size());
-        for (uint32_t e = g.first[u]; e < g.first[u] + deg; ++e) {
-            const uint32_t c = g.dst[e];
-            new_slot(c, slot_of_node[c] != kUnplaced);
-        }
-        child_base[head] = run;
+    std::vector<uint64_t> ref_base, made; // per head of the level: first reference, first new slot
+    std::vector<uint8_t> prim;            // per reference of the level: places its child's primary
+    for (size_t h0 = 0; h0 < node_of_slot.size();) {
+        const size_t h1 = node_of_slot.size(), L = h1 - h0;
+        auto degree = [&](size_t i) -> uint32_t { return copy_slot[h0 + i] ? 0u : g.degree[node_of_slot[h0 + i]]; };
+        ref_base.assign(L + 1, 0);
+        for (size_t i = 0; i < L; ++i) ref_base[i + 1] = ref_base[i] + degree(i);
+        const uint64_t R = ref_base[L];
+        if (R >= kUnplaced) fail(HEPFAC_ERR_INTERNAL, "trie level exceeds 2^32 references");
+        // 1. first reference of every unplaced child
+        parallel_slices(L, kGrain, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) {
+                const uint32_t d = degree(i);
+                const uint32_t f = d ? g.first[node_of_slot[h0 + i]] : 0u;
+                for (uint32_t k = 0; k < d; ++k) {
+                    const uint32_t c = g.dst[f + k];
+                    if (slot_of_node[c] != kUnplaced) continue;
+                    const uint32_t r = uint32_t(ref_base[i] + k);
+                    std::atomic_ref<uint32_t> m(first_ref[c]);
+                    uint32_t cur = m.load(std::memory_order_relaxed);
+                    while (r < cur && !m.compare_exchange_weak(cur, r, std::memory_order_relaxed)) {
+                    }
+                }
+            }
+        });
+        // 2. which references place a primary, and how many slots each head makes
+        prim.assign(size_t(R), 0);
+        made.assign(L + 1, 0);
+        parallel_slices(L, kGrain, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) {
+                const uint32_t d = degree(i);
+                const uint32_t f = d ? g.first[node_of_slot[h0 + i]] : 0u;
+                for (uint32_t k = 0; k < d; ++k) {
+                    const uint32_t c = g.dst[f + k];
+                    prim[ref_base[i] + k] = slot_of_node[c] == kUnplaced && first_ref[c] == uint32_t(ref_base[i] + k);
+                }
+                made[i + 1] = d > 1 ? d : (d == 1 ? prim[ref_base[i]] : 0u);
+            }
+        });
+        for (size_t i = 0; i < L; ++i) made[i + 1] += made[i];
+        const uint64_t total = h1 + made[L];
+        if (total > Trie::kMaxNodes) fail(HEPFAC_ERR_INTERNAL, "trie exceeds 2^31-1 nodes");
+        node_of_slot.resize(total);
+        copy_slot.resize(total);
+        child_base.resize(total, 0);
+        // 3. create the level's slots; single children placed here are linked
+        parallel_slices(L, kGrain, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) {
+                const uint32_t d = degree(i);
+                if (d == 0) continue;
+                const uint32_t f = g.first[node_of_slot[h0 + i]];
+                const uint32_t base = uint32_t(h1 + made[i]);
+                if (d == 1 && !prim[ref_base[i]]) continue; // linked in step 4
+                child_base[h0 + i] = base;
+                for (uint32_t k = 0; k < d; ++k) {
+                    const uint32_t c = g.dst[f + k], slot = base + k;
+                    const bool p = prim[ref_base[i] + k];
+                    node_of_slot[slot] = c;
+                    copy_slot[slot] = p ? 0 : 1;
+                    if (p) slot_of_node[c] = slot;
+                }
+            }
+        });
+        // 4. single children placed earlier, or by another head of this level
+        parallel_slices(L, kGrain, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i)
+                if (degree(i) == 1 && !prim[ref_base[i]])
+                    child_base[h0 + i] = slot_of_node[g.dst[g.first[node_of_slot[h0 + i]]]];
+        });
+        h0 = h1;
     }
-    // Note: primary slots are appended in discovery order and the loop above
-    // visits them in that same order, which is exactly a FIFO queue of
-    // primaries (copies are skipped).
 
     auto t = std::make_unique<Trie>(like.alphabet);
     t->node_count = uint32_t(node_of_slot.size());
     const uint32_t stride = t->stride();
-    t->cells.assign(size_t(t->node_count) * stride, 0);
-    for (uint32_t s = 0; s < t->node_count; ++s) {
-        const uint32_t u = node_of_slot[s];
-        uint32_t* c = t->cells.data() + size_t(s) * stride;
-        for (uint32_t e = g.first[u]; e < g.first[u] + g.degree[u]; ++e)
-            c[g.sym[e] >> 5] |= 1u << (g.sym[e] & 31u);
-        const uint32_t src = copy_slot[s] ? slot_of_node[u] : s;
-        c[t->words] = (child_base[src] & Trie::kOffsetMask) | (g.term[u] ? Trie::kTerminal : 0u);
-    }
+    t->cells.resize(size_t(t->node_count) * stride); // uninitialised: every word is written below
+    parallel_slices(t->node_count, 1 << 16, [&](size_t b, size_t e) {
+        for (size_t s = b; s < e; ++s) {
+            const uint32_t u = node_of_slot[s];
+            uint32_t* c = t->cells.data() + s * stride;
+            std::fill(c, c + t->words, 0u);
+            for (uint32_t e2 = g.first[u]; e2 < g.first[u] + g.degree[u]; ++e2)
+                c[g.sym[e2] >> 5] |= 1u << (g.sym[e2] & 31u);
+            const uint32_t src = copy_slot[s] ? slot_of_node[u] : uint32_t(s);
+            c[t->words] = (child_base[src] & Trie::kOffsetMask) | (g.term[u] ? Trie::kTerminal : 0u);
+        }
+    });
     t->patterns = like.patterns;
     t->set_lengths();
     t->stage = stage;

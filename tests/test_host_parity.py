@@ -238,6 +238,29 @@ def test_layouts_equal_reference(lib, ref, sigma):
                 assert nL == nR and xL.save_bytes() == xR.save_bytes()
 
 
+@pytest.mark.parametrize("threads", ["1", "8"])
+def test_large_layouts_equal_reference(lib, ref, threads, monkeypatch):
+    # Level-parallel BFS emission (trie.cpp emit): BFS levels of 10^4-10^5
+    # slots are split over the host threads; the emitted layout must equal
+    # the reference's queue order byte for byte (trie.cpp:133-217), and be
+    # independent of the thread count.  Config 5 at 100k patterns (sigma
+    # 256) and a dense sigma=4 set (DAG merges across long chains).
+    monkeypatch.setenv("HEPFAC_COMPILER_THREADS", threads)
+    rng = np.random.default_rng(11)
+    cases = [(256, workloads.config("c5", count=100_000).patterns)]
+    syms = np.frombuffer(b"ACGT", dtype=np.uint8)
+    cases.append((4, pattern_set(rng, syms, 60_000, 8, 24)))
+    for sigma, pats in cases:
+        aL, aR = lib.alphabet(sigma), ref.alphabet(sigma)
+        tL, tR = lib.build_trie(lib.patterns(pats, aL)), ref.build_trie(ref.patterns(pats, aR))
+        assert tL.save_bytes() == tR.save_bytes()
+        s1L, s1R = tL.compress(1)[0], tR.compress(1)[0]
+        assert s1L.save_bytes() == s1R.save_bytes()
+        assert tL.compress(2)[0].save_bytes() == tR.compress(2)[0].save_bytes()
+        for d in (4, 9):
+            assert s1L.truncate(d)[0].save_bytes() == s1R.truncate(d)[0].save_bytes()
+
+
 def test_generators_equal_reference(lib, ref):
     for sigma in (2, 4, 52, 256):
         aL, aR = lib.alphabet(sigma), ref.alphabet(sigma)
