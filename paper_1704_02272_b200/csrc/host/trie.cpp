@@ -198,26 +198,37 @@ Graph graph_of(const Trie& t)
     g.first.resize(n);
     g.degree.resize(n);
     g.term.resize(n);
+    // degrees, then edge offsets by a prefix sum, then the edges: each pass
+    // on all host threads
+    parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+        for (size_t u = b; u < e; ++u) {
+            g.degree[u] = t.child_count(uint32_t(u));
+            g.term[u] = (t.cell(uint32_t(u))[t.words] & Trie::kTerminal) ? 1 : 0;
+        }
+    });
     size_t edges = 0;
-    for (uint32_t u = 0; u < n; ++u) edges += t.child_count(u);
-    g.sym.reserve(edges);
-    g.dst.reserve(edges);
     for (uint32_t u = 0; u < n; ++u) {
-        const uint32_t* c = t.cell(u);
-        g.first[u] = uint32_t(g.dst.size());
-        g.term[u] = (c[t.words] & Trie::kTerminal) ? 1 : 0;
-        uint32_t target = c[t.words] & Trie::kOffsetMask;
-        for (uint32_t w = 0; w < t.words; ++w) {
-            uint32_t bits = c[w];
-            while (bits) {
-                uint32_t b = uint32_t(__builtin_ctz(bits));
-                bits &= bits - 1;
-                g.sym.push_back(uint16_t(w * 32 + b));
-                g.dst.push_back(target++);
+        g.first[u] = uint32_t(edges);
+        edges += g.degree[u];
+    }
+    g.sym.resize(edges);
+    g.dst.resize(edges);
+    parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+        for (size_t u = b; u < e; ++u) {
+            const uint32_t* c = t.cell(uint32_t(u));
+            uint32_t target = c[t.words] & Trie::kOffsetMask;
+            size_t at = g.first[u];
+            for (uint32_t w = 0; w < t.words; ++w) {
+                uint32_t bits = c[w];
+                while (bits) {
+                    const uint32_t bit = uint32_t(__builtin_ctz(bits));
+                    bits &= bits - 1;
+                    g.sym[at] = uint16_t(w * 32 + bit);
+                    g.dst[at++] = target++;
+                }
             }
         }
-        g.degree[u] = uint32_t(g.dst.size()) - g.first[u];
-    }
+    });
     return g;
 }
 
@@ -414,7 +425,14 @@ std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
         return key;
     };
 
-    std::unordered_map<uint32_t, uint32_t> rep_of_suffix; // suffix -> representative node
+    // suffix -> representative node, directly indexed (2^24 + 2^16 + 2^8 slots)
+    auto suffix_index = [](uint32_t key) -> size_t {
+        const uint32_t k = key >> 24;
+        if (k == 3) return key & 0xFFFFFFu;
+        if (k == 2) return (size_t(1) << 24) + ((key >> 8) & 0xFFFFu);
+        return (size_t(1) << 24) + (size_t(1) << 16) + ((key >> 16) & 0xFFu);
+    };
+    std::vector<uint32_t> rep_of_suffix((size_t(1) << 24) + (size_t(1) << 16) + 256, Trie::kNone);
     std::vector<std::pair<uint32_t, uint32_t>> reps;      // (node, suffix) in creation order
     std::vector<std::pair<uint32_t, uint32_t>> rewires;   // (parent, new only child)
     // Phase A (parallel, per pattern): its path's last nodes and the length
@@ -468,18 +486,19 @@ std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
         const uint32_t* node = tails[i].node; // node[k] = path[L - k]
         uint32_t replace = 0; // deepest level whose class already has another owner
         for (uint32_t k = chain; k >= 1; --k) {
-            auto it = rep_of_suffix.find(suffix_key(p, k));
-            if (it != rep_of_suffix.end() && it->second != node[k]) {
+            const uint32_t rep = rep_of_suffix[suffix_index(suffix_key(p, k))];
+            if (rep != Trie::kNone && rep != node[k]) {
                 replace = k;
                 break;
             }
         }
         for (uint32_t k = replace + 1; k <= chain; ++k) {
             const uint32_t key = suffix_key(p, k);
-            if (rep_of_suffix.emplace(key, node[k]).second) reps.emplace_back(node[k], key);
+            uint32_t& rep = rep_of_suffix[suffix_index(key)];
+            if (rep == Trie::kNone) rep = node[k], reps.emplace_back(node[k], key);
         }
         if (replace >= 1)
-            rewires.emplace_back(node[replace + 1], rep_of_suffix.at(suffix_key(p, replace)));
+            rewires.emplace_back(node[replace + 1], rep_of_suffix[suffix_index(suffix_key(p, replace))]);
     }
 
     // Representatives of k-suffixes point at the representative of their
@@ -489,8 +508,8 @@ std::unique_ptr<Trie> merge_tail_chains(const Trie& t, CompressionStats* stats)
         if (k < 2) continue;
         // drop the first byte: shift the remaining k-1 bytes up one position
         const uint32_t sub = ((k - 1) << 24) | ((key << 8) & 0x00FFFF00u);
-        auto it = rep_of_suffix.find(sub);
-        if (it != rep_of_suffix.end()) g.dst[g.first[node]] = it->second;
+        const uint32_t rep = rep_of_suffix[suffix_index(sub)];
+        if (rep != Trie::kNone) g.dst[g.first[node]] = rep;
     }
     for (const auto& [parent, child] : rewires) g.dst[g.first[parent]] = child;
 
