@@ -25,8 +25,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <unordered_map>
-#include <unordered_set>
 
 namespace hfb {
 
@@ -163,33 +161,55 @@ void build_jump_table(GpuImage& im, const std::vector<JumpEntry>& entries, const
 std::vector<InlineList> inline_lists(const Trie& t, const GpuImage& im, std::vector<JumpEntry>& entries,
                                      const std::vector<uint64_t>& keys, uint32_t k, uint32_t sb)
 {
-    std::unordered_map<uint64_t, uint32_t> at;
-    at.reserve(keys.size() * 2);
-    for (size_t i = 0; i < keys.size(); ++i) at.emplace(keys[i], uint32_t(i));
-    std::vector<std::vector<uint32_t>> ids(keys.size());
-    for (size_t id = 0; id < t.patterns.size(); ++id) {
-        const auto& p = t.patterns[id];
-        if (p.size() < k) return {}; // cannot happen when k <= min_emit; stay on the walk
-        uint64_t key = 0;
-        for (uint32_t i = 0; i < k; ++i) {
-            const uint8_t c = uint8_t(p[i]);
-            key |= sb ? uint64_t(uint32_t(t.alphabet.symbol_of(c))) << (sb * i) : uint64_t(c) << (8 * i);
+    const size_t K = keys.size(), P = t.patterns.size();
+    // the keys sorted (each once: the trie spells a string by one path), for
+    // binary-search lookups from all host threads
+    std::vector<std::pair<uint64_t, uint32_t>> sorted(K);
+    for (size_t i = 0; i < K; ++i) sorted[i] = {keys[i], uint32_t(i)};
+    std::sort(sorted.begin(), sorted.end());
+    std::vector<uint32_t> key_of(P);
+    std::atomic<bool> off{false};
+    parallel_slices(P, 4096, [&](size_t b, size_t e) {
+        for (size_t id = b; id < e; ++id) {
+            const auto& p = t.patterns[id];
+            if (p.size() < k) { // cannot happen when k <= min_emit; stay on the walk
+                off = true;
+                return;
+            }
+            uint64_t key = 0;
+            for (uint32_t i = 0; i < k; ++i) {
+                const uint8_t c = uint8_t(p[i]);
+                key |= sb ? uint64_t(uint32_t(t.alphabet.symbol_of(c))) << (sb * i) : uint64_t(c) << (8 * i);
+            }
+            const auto it = std::lower_bound(sorted.begin(), sorted.end(), std::make_pair(key, 0u));
+            if (it == sorted.end() || it->first != key) { // a pattern off the trie: not its dictionary
+                off = true;
+                return;
+            }
+            key_of[id] = it->second;
         }
-        auto it = at.find(key);
-        if (it == at.end()) return {}; // a pattern off the trie: not its dictionary
-        if (ids[it->second].size() <= kJumpExtEntries) ids[it->second].push_back(uint32_t(id));
-    }
-    std::vector<InlineList> lists(keys.size());
-    for (size_t i = 0; i < keys.size(); ++i) {
-        lists[i].fill(kNoId);
-        auto& v = ids[i];
-        if (v.empty() || v.size() > kJumpExtEntries) continue;
-        std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
-            return im.pat_len[x] != im.pat_len[y] ? im.pat_len[x] < im.pat_len[y] : x < y;
-        });
-        std::copy(v.begin(), v.end(), lists[i].begin());
-        entries[i][6] |= kJumpInline | (uint32_t(v.size()) << kJumpInlineShift);
-    }
+    });
+    if (off) return {};
+    // every key's patterns in id order (counting sort)
+    std::vector<uint32_t> first(K + 1, 0);
+    for (size_t id = 0; id < P; ++id) ++first[key_of[id] + 1];
+    for (size_t i = 0; i < K; ++i) first[i + 1] += first[i];
+    std::vector<uint32_t> flat(P), next(first.begin(), first.end() - 1);
+    for (size_t id = 0; id < P; ++id) flat[next[key_of[id]]++] = uint32_t(id);
+    std::vector<InlineList> lists(K);
+    parallel_slices(K, 1 << 14, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            lists[i].fill(kNoId);
+            const uint32_t n = first[i + 1] - first[i];
+            if (n == 0 || n > kJumpExtEntries) continue;
+            uint32_t* v = flat.data() + first[i];
+            std::sort(v, v + n, [&](uint32_t x, uint32_t y) {
+                return im.pat_len[x] != im.pat_len[y] ? im.pat_len[x] < im.pat_len[y] : x < y;
+            });
+            std::copy(v, v + n, lists[i].begin());
+            entries[i][6] |= kJumpInline | (n << kJumpInlineShift);
+        }
+    });
     return lists;
 }
 
@@ -214,11 +234,14 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     // Structural validation: a loaded .htri is only checked for offset < n by
     // the format (reference trie_io.cpp:155-159); child runs must fit too.
     std::vector<uint32_t> kids(n);
-    for (uint32_t u = 0; u < n; ++u) {
-        kids[u] = t.child_count(u);
-        if (kids[u] && uint64_t(t.offset(u)) + kids[u] > n)
-            fail(HEPFAC_ERR_FORMAT, "trie file offset out of range (child run past the node array)");
-    }
+    std::atomic<bool> past{false};
+    parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+        for (size_t u = b; u < e; ++u) {
+            kids[u] = t.child_count(uint32_t(u));
+            if (kids[u] && uint64_t(t.offset(uint32_t(u))) + kids[u] > n) past = true;
+        }
+    });
+    if (past) fail(HEPFAC_ERR_FORMAT, "trie file offset out of range (child run past the node array)");
 
     phase(0);
     // ---- alphabet --------------------------------------------------------
@@ -244,21 +267,21 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     std::vector<uint64_t> keys(P);
     for (uint64_t attempt = 0;; ++attempt) {
         im.hmul = 0x100000001B3ull + 2 * attempt * 0x9E3779B97F4A7C15ull; // odd multipliers
-        std::unordered_set<uint64_t> seen;
-        seen.reserve(P * 2);
-        bool unique = true;
-        for (size_t i = 0; i < P && unique; ++i) {
-            const std::string& p = t.patterns[i];
-            uint64_t h = 0;
-            for (size_t o = 0; o < p.size(); o += 4) {
-                uint32_t w = 0;
-                for (size_t b = 0; b < 4 && o + b < p.size(); ++b) w |= uint32_t(uint8_t(p[o + b])) << (8 * b);
-                h = slice_step(h, im.hmul, w);
+        parallel_slices(P, 4096, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) {
+                const std::string& p = t.patterns[i];
+                uint64_t h = 0;
+                for (size_t o = 0; o < p.size(); o += 4) {
+                    uint32_t w = 0;
+                    for (size_t c = 0; c < 4 && o + c < p.size(); ++c) w |= uint32_t(uint8_t(p[o + c])) << (8 * c);
+                    h = slice_step(h, im.hmul, w);
+                }
+                keys[i] = slice_key(h, uint32_t(p.size()));
             }
-            keys[i] = slice_key(h, uint32_t(p.size()));
-            unique = seen.insert(keys[i]).second;
-        }
-        if (unique) break;
+        });
+        std::vector<uint64_t> sorted(keys);
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end()) break;
         if (attempt > 64) fail(HEPFAC_ERR_INTERNAL, "cannot find collision-free slice keys");
     }
     const uint64_t slots = uint64_t(1) << std::max<uint32_t>(4, ceil_log2(2 * P + 1));
@@ -275,8 +298,11 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     phase(2);
     // ---- terminal ids: baked in where the node spells exactly one string ----
     std::vector<uint32_t> indeg(n, 0);
-    for (uint32_t u = 0; u < n; ++u)
-        for (uint32_t i = 0; i < kids[u]; ++i) indeg[t.offset(u) + i]++;
+    parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
+        for (size_t u = b; u < e; ++u)
+            for (uint32_t i = 0; i < kids[u]; ++i)
+                std::atomic_ref<uint32_t>(indeg[t.offset(uint32_t(u)) + i]).fetch_add(1, std::memory_order_relaxed);
+    });
     std::vector<uint8_t> unique_path(n, 0);
     {
         std::vector<uint32_t> q{0};
@@ -607,7 +633,8 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                 const uint32_t N = 1u << 15;
                 uint64_t x = 0x9E3779B97F4A7C15ull;
                 uint32_t n_single = 0, n_first = 0, n_both = 0, n_true = 0;
-                const std::unordered_set<uint64_t> paths(grams.begin(), grams.end());
+                std::vector<uint64_t> paths(grams);
+                std::sort(paths.begin(), paths.end());
                 auto word_bit = [](const std::vector<uint32_t>& tab, uint32_t word, uint32_t byte) {
                     return (tab[word] & filter_mask_bit(byte)) != 0;
                 };
@@ -619,7 +646,7 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
                     }
                     const uint32_t k32 = filter_fold(key);
                     n_single += word_bit(single, filter_word(k32, bits - 5), k32);
-                    n_true += paths.count(key) ? 1u : 0u;
+                    n_true += std::binary_search(paths.begin(), paths.end(), key) ? 1u : 0u;
                     if (k >= 4) {
                         const uint32_t p = uint32_t(key);
                         const bool a = word_bit(pair, pair_word(p >> 8, pair_wb), p & 0xFFu);
