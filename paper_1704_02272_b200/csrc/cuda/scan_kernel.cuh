@@ -607,12 +607,12 @@ __device__ __forceinline__ void emit_at_limit(const ScanArgs& a, const JumpHit& 
 // L1 hits next to the window just read.  Pattern bytes are read only past
 // those 24.
 template <class S>
-__device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h, uint64_t start, S& sink)
+__device__ __forceinline__ void emit_inline(const ScanArgs& a, uint32_t slot, uint32_t flags, uint64_t start, S& sink)
 {
     const TrieView& t = a.trie;
     const uint32_t skip = inline_skip(t.filter_k, t.sym_bits);
-    const uint4* ext = reinterpret_cast<const uint4*>(t.jump_ext) + 4 * h.slot;
-    const uint32_t cnt = (h.aux.z >> kJumpInlineShift) & 3u;
+    const uint4* ext = reinterpret_cast<const uint4*>(t.jump_ext) + 4 * slot;
+    const uint32_t cnt = (flags >> kJumpInlineShift) & 3u;
     uint4 x[4];
     x[0] = __ldg(ext);
     x[1] = __ldg(ext + 1);
@@ -645,11 +645,14 @@ __device__ __forceinline__ void emit_inline(const ScanArgs& a, const JumpHit& h,
 }
 
 // The walking pass (32 warps, 64 registers) keeps the inline check out of
-// line: few of its candidates reach a slot, and inlined it spilled.
+// line: few of its candidates reach a slot, and inlined it spilled.  The
+// sink goes in and comes back by value, so the caller's sink stays in
+// registers (by reference it had to live in local memory for the whole walk).
 template <class S>
-__device__ __noinline__ void emit_inline_call(const ScanArgs& a, const JumpHit& h, uint64_t start, S& sink)
+__device__ __noinline__ S emit_inline_call(const ScanArgs& a, uint32_t slot, uint32_t flags, uint64_t start, S sink)
 {
-    emit_inline(a, h, start, sink);
+    emit_inline(a, slot, flags, start, sink);
+    return sink;
 }
 
 template <bool PAR, class S>
@@ -657,11 +660,11 @@ __device__ __forceinline__ void emit_listed(const ScanArgs& a, const JumpHit& h,
 {
 #ifndef HFB_INLINE_ALL
     if (PAR) {
-        emit_inline_call(a, h, start, sink);
+        sink = emit_inline_call(a, h.slot, h.aux.z, start, sink);
         return;
     }
 #endif
-    emit_inline(a, h, start, sink);
+    emit_inline(a, h.slot, h.aux.z, start, sink);
 }
 
 template <bool GROUPED, bool IDENT, int KW, bool PAR, class S>
@@ -975,13 +978,9 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
             pre -= cnt; // exclusive
             if (total <= kQueue) {
                 // every entry of the unit loaded at once: entry f belongs to
-                // the last tile i with pre_i <= f
-                uint32_t pres[kSuper], slots[kSuper];
-#pragma unroll
-                for (uint32_t i = 0; i < kSuper; ++i) {
-                    pres[i] = __shfl_sync(0xFFFFFFFFu, pre, i);
-                    slots[i] = __shfl_sync(0xFFFFFFFFu, cslot, i);
-                }
+                // the last tile i with pre_i <= f (lane i < kSuper holds
+                // pre_i and tile i's slot; a 3-step search over shuffles)
+                static_assert(kSuper == 8, "the tile search takes 3 steps");
                 // Entries are re-checked against the 4-byte-prefix bitmap
                 // (one shared-memory probe) and compacted in order: most
                 // pair survivors are false positives, and each would cost
@@ -993,14 +992,12 @@ __global__ void __launch_bounds__(CANDS ? kCWarps * 32 : kThreads, 1) pfac_scan_
                     const uint32_t f = f0 + lane;
                     bool keep = false;
                     uint16_t v = 0;
+                    uint32_t i = 0;
+#pragma unroll
+                    for (uint32_t step = kSuper / 2; step; step >>= 1)
+                        if (f >= __shfl_sync(0xFFFFFFFFu, pre, i + step)) i += step;
+                    const uint32_t p_i = __shfl_sync(0xFFFFFFFFu, pre, i), s_i = __shfl_sync(0xFFFFFFFFu, cslot, i);
                     if (f < total) {
-                        uint32_t i = 0;
-#pragma unroll
-                        for (uint32_t k = 1; k < kSuper; ++k) i += f >= pres[k] ? 1u : 0u;
-                        uint32_t p_i = pres[0], s_i = slots[0];
-#pragma unroll
-                        for (uint32_t k = 1; k < kSuper; ++k)
-                            if (i == k) p_i = pres[k], s_i = slots[k];
                         const uint64_t t_i = unit * kSuper + i;
                         const uint64_t at = (t_i % a.cand_warps) * a.cand_cap + s_i + (f - p_i);
                         v = uint16_t(a.cand[at] + i * kTile);
