@@ -18,8 +18,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <chrono>
-#include <cstdio>
 #include <array>
 #include <cmath>
 #include <cstdlib>
@@ -38,14 +36,6 @@ size_t GpuImage::device_bytes() const
 ImageOptions image_options_from_env()
 {
     ImageOptions o;
-    if (const char* s = std::getenv("HEPFAC_FILTER_BITS_MAX")) {
-        long v = std::strtol(s, nullptr, 10);
-        if (v >= 10 && v <= 20) o.max_filter_bits = uint32_t(v);
-    }
-    if (const char* s = std::getenv("HEPFAC_FILTER_SLACK")) {
-        long v = std::strtol(s, nullptr, 10);
-        if (v >= 0 && v <= 10) o.filter_slack = uint32_t(v);
-    }
     if (const char* s = std::getenv("HEPFAC_JUMP")) o.jump = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_JUMP_EXT")) o.jump_ext = std::strtol(s, nullptr, 10) != 0;
     if (const char* s = std::getenv("HEPFAC_SYMBOL_KEYS")) o.symbol_keys = std::strtol(s, nullptr, 10) != 0;
@@ -53,10 +43,6 @@ ImageOptions image_options_from_env()
     if (const char* s = std::getenv("HEPFAC_FILTER_MODE")) {
         const std::string m = s;
         o.filter_mode = m == "single" ? 1u : (m == "pair" ? 2u : (m == "l2" ? 4u : 0u));
-    }
-    if (const char* s = std::getenv("HEPFAC_FILTER2_SLACK")) {
-        long v = std::strtol(s, nullptr, 10);
-        if (v >= 0 && v <= 16) o.filter2_slack = uint32_t(v);
     }
     return o;
 }
@@ -217,15 +203,6 @@ std::vector<InlineList> inline_lists(const Trie& t, const GpuImage& im, std::vec
 
 GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
 {
-    // HEPFAC_IMAGE_TIMING=1: per-phase wall times on stderr (tuning only)
-    const bool timing = std::getenv("HEPFAC_IMAGE_TIMING") != nullptr;
-    auto t_last = std::chrono::steady_clock::now();
-    auto phase = [&](int k) {
-        if (!timing) return;
-        const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "image phase %d: %.3f s\n", k - 1, std::chrono::duration<double>(now - t_last).count());
-        t_last = now;
-    };
     GpuImage im;
     const uint32_t n = t.node_count;
     if (n >= kMaxGpuNodes) fail(HEPFAC_ERR_NOMEM, "trie too large for the GPU image (>= 2^30 nodes)");
@@ -243,7 +220,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     });
     if (past) fail(HEPFAC_ERR_FORMAT, "trie file offset out of range (child run past the node array)");
 
-    phase(0);
     // ---- alphabet --------------------------------------------------------
     im.identity = t.alphabet.is_identity();
     for (unsigned b = 0; b < 256; ++b) {
@@ -252,7 +228,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     }
     im.depth_limit = t.depth_limit.value_or(0);
 
-    phase(1);
     // ---- dictionary + slice-key table -------------------------------------
     const size_t P = t.patterns.size();
     im.pat_off.resize(P);
@@ -295,7 +270,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         im.ht_id[s] = uint32_t(i);
     }
 
-    phase(2);
     // ---- terminal ids: baked in where the node spells exactly one string ----
     std::vector<uint32_t> indeg(n, 0);
     parallel_slices(n, 1 << 16, [&](size_t b, size_t e) {
@@ -332,7 +306,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     });
 
-    phase(3);
     // ---- path ids: keyed terminals named by the walk's path ------------------
     // A pattern whose terminal is shared (keyed) is still determined by the
     // deepest path-unique node U on its path when U leads to no other keyed
@@ -435,7 +408,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     // the path id a walk carries after entering node v from a parent carrying `pend`
     auto pend_at = [&](uint32_t v, uint32_t pend) { return im.path_id[v] != kKeep ? im.path_id[v] : pend; };
 
-    phase(4);
     // ---- buckets: CSR, each sorted by (length, id) -----------------------
     im.bucket_of.assign(n, kNoId);
     for (const auto& [node, ids] : t.buckets) {
@@ -457,7 +429,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
     if (im.bk_span.empty()) im.bk_span.assign(2, 0);
     if (im.bk_entry.empty()) im.bk_entry.assign(4, 0);
 
-    phase(5);
     // ---- node records ------------------------------------------------------
     const uint32_t sigma = t.alphabet.size();
     im.groups = sigma <= 32 ? 0 : (sigma + 63) / 64;
@@ -492,7 +463,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         });
     }
 
-    phase(6);
     // ---- report depths: min_emit (BFS) -------------------------------------
     {
         std::vector<uint32_t> depth(n, UINT32_MAX), q{0};
@@ -513,7 +483,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         if (im.depth_limit && !t.buckets.empty()) im.min_emit = std::min(im.min_emit, im.depth_limit);
     }
 
-    phase(7);
     // ---- reach: longest root path (cyclic => unbounded), plus buckets ------
     if (im.depth_limit) {
         uint64_t r = im.depth_limit;
@@ -558,7 +527,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         im.reach = cyclic ? UINT64_MAX : longest[0];
     }
 
-    phase(8);
     // ---- start filter --------------------------------------------------------
     if (im.min_emit != UINT32_MAX) {
         const uint32_t k = std::min(im.min_emit, kMaxFilterKey);
@@ -760,7 +728,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     }
 
-    phase(9);
     // ---- symbol-key mode (small alphabets) -----------------------------------
     // Byte keys carry log2(sigma) bits per byte: 8 bytes of DNA are 16 bits, of
     // a binary alphabet 8.  When the shortest report depth allows more than 8
@@ -847,7 +814,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
             }
         }
     }
-    phase(10);
     // ---- direct-index form (filter mode 5, layout.hpp) -------------------------
     // Alphabets of at most 4 symbols whose every pattern has 8..32 symbols
     // (c2: DNA, 10k patterns of 8-32): the byte-key path filters on 8-byte
@@ -923,7 +889,6 @@ GpuImage build_gpu_image(const Trie& t, const ImageOptions& opt)
         }
     }
 
-    phase(11);
     if (im.filter.empty()) im.filter.push_back(0);
     if (im.filter2.empty()) im.filter2.push_back(0);
     if (im.jump.empty()) im.jump.assign(kJumpWords, 0u), im.jump_ext.clear();
