@@ -188,3 +188,55 @@ def test_reference_arm_under_torchrun():
     if "unavailable" not in line:
         assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
         assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
+
+
+def _gpu_worker(rank, world, port, q, per_rank):
+    # As _workload_worker, but every rank scans its shard with the product
+    # (hepfac_b200_scan_shard on the GPU); the ranks share one device, the
+    # count exchange goes over gloo.  Nothing waits across ranks on the GPU.
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1704_02272_b200 import hepfac, workloads
+        lib = hepfac.lib()
+        w = workloads.config("c1")
+        t, _ = workloads.build_trie(lib, w, "s1trunc")
+        shard = D.plan(per_rank * world, world, rank, lib.halo(t))
+        mine = w.make_text(shard.nbytes, lo=shard.lo)
+        recs, off, total = D.scan_sharded(mine, shard, lambda b, lo, owned: lib.scan_shard(t, b, lo, owned))
+        launches = lib.last_scan_stats()["kernel_launches"]
+        allrecs = D.gather_all(recs)
+        q.put((rank, off, total, launches, allrecs.tobytes() if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_workload_equals_reference():
+    # the product's shard scans, placed by the count exchange,
+    # concatenate to the reference's whole-text list (scan.cpp:104-111).
+    import oracle
+    ref = oracle.ref_library()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    from paper_1704_02272_b200 import workloads
+    world, per_rank = 2, (24 << 20) + 5  # the seam inside a 16 MiB block
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, per_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w = workloads.config("c1")
+    rt, _ = workloads.build_trie(ref, w, "s1trunc")
+    want = ref.scan(rt, w.make_text(per_rank * world), workers=os.cpu_count() or 4)
+    assert all(r[3] >= 1 for r in results)  # GPU kernels ran on every rank
+    assert {r[2] for r in results} == {want.size}
+    got = np.frombuffer(results[0][4], dtype=want.dtype)
+    assert got.tobytes() == want.tobytes() and want.size > 5000
