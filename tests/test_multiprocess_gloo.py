@@ -5,8 +5,9 @@ is the C oracle or the compiled reference restricted to the shard's starts;
 the shard and halo arithmetic (the halo from the product library), the global
 block text, the count exchange and the ordering are what is under test.  The
 GPU scan_shard itself is checked against whole-text scans in
-test_gpu_parity.py, and bench.py --check compares the rank-order
-concatenation with a one-rank scan on the GPU box."""
+test_gpu_parity.py, bench.py --check compares the rank-order
+concatenation with a one-rank scan on the GPU box, and the gpu-marked test
+at the end runs two ranks whose scanner is the product itself."""
 import os
 import socket
 
