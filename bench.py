@@ -254,7 +254,7 @@ def main():
     ap.add_argument("--count", type=int, default=0, help="config c5 pattern count")
     ap.add_argument("--cpu-sample-bytes", type=int, default=256 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 5), raised to cover >= 4 GiB of text (at most 50)")
     ap.add_argument("--check", action="store_true",
                     help="compare the rank-order concatenation of the shard lists with a one-rank scan (SHA-256)")
     args = ap.parse_args()
@@ -350,7 +350,10 @@ def main():
         host[:] = text
     except Exception:
         host = text
-    e2e_steps = args.e2e_steps or min(args.steps, 5)
+    # at least ~4 GiB of text per rank over the e2e window (5 scans of the
+    # 4 GiB contract text; 20 of a 1 GiB config), so one host-side hiccup
+    # does not swing a short window (at most 50 scans)
+    e2e_steps = args.e2e_steps or max(min(args.steps, 5), min(50, -(-(4 << 30) // max(1, owned))))
 
     def e2e_run(buf):
         # view=True: the records stay in the library's (pinned) list, as a C
